@@ -1,0 +1,129 @@
+/*
+ * psmooth.h -- C ABI of libpsmooth.so, the B200 (sm_100a) block-relaxation
+ * smoother for the constant-coefficient 7-point stencil.
+ *
+ * The reference (patchsmooth 0.1.0, pure Python/numpy) has no FFI; its seam is
+ * the Python smoother API.  Each entry point below replaces one reference
+ * function on the hot path (cited per declaration, paths relative to
+ * /root/reference/pkg/src/patchsmooth/).  The Python package
+ * paper_1208_1975_b200 keeps the reference's names and signatures and calls
+ * these through ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Every function returns 0 on success, a negative psm_status otherwise;
+ *    psm_last_error() returns a thread-local message for the last failure.
+ *  - All device work is asynchronous and ordered on the caller's stream
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Field memory is owned by the caller (torch).  The library receives raw
+ *    device pointers and never frees them.  Plans own only factor tables,
+ *    device patch/copy tables, progress flags and reduction workspace.
+ *  - Layout: patch buffers are (nx+2)*(ny+2)*(nz+2) doubles, x fastest
+ *    (numpy F-order (nx+2,ny+2,nz+2) == torch C-contiguous (nz+2,ny+2,nx+2)),
+ *    exactly the reference layout (grid.py:153-182); f is nx*ny*nz, x fastest.
+ */
+#ifndef PSMOOTH_H
+#define PSMOOTH_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum psm_status {
+  PSM_OK = 0,
+  PSM_EINVAL = -1,    /* invalid argument (maps to ValueError)        */
+  PSM_ESINGULAR = -2, /* block operator singular / not dominant       */
+  PSM_ECUDA = -3,     /* CUDA runtime failure (maps to RuntimeError)  */
+  PSM_ENOMEM = -4,    /* device or host allocation failed             */
+  PSM_EUNSUPPORTED = -5
+};
+
+enum psm_block_kind { PSM_BLOCK_LINE = 1, PSM_BLOCK_PLANE = 2 };
+
+enum psm_gs_mode {
+  PSM_GS_WAVEFRONT = 0, /* deterministic: == lexicographic block GS (runtime.py:164-168) */
+  PSM_GS_CHAOTIC = 1    /* in place, no ordering between concurrent lines (runtime.py:185-196) */
+};
+
+/* stencil.py:52-68 Stencil7: center > 0, faces in order -x,+x,-y,+y,-z,+z */
+typedef struct {
+  double center;
+  double faces[6];
+} psm_stencil;
+
+/* grid.py:153-217 Patch: both padded buffers plus interior f (device pointers) */
+typedef struct {
+  double* buf[2];
+  double* f;
+  int nx, ny, nz;
+} psm_patch_desc;
+
+/* grid.py:333-352 InterfaceCopy: src interior layer -> dst ghost layer */
+typedef struct {
+  int src, dst;
+  int src_lo[3], dst_lo[3], extent[3];
+} psm_copy_desc;
+
+typedef struct psm_factors psm_factors;
+typedef struct psm_plan psm_plan;
+
+const char* psm_last_error(void);
+int psm_version(void);
+
+/* ---- factor tables (replaces InverseCache.get -> assemble_block_matrix ->
+ *      invert_dense, blocklinalg.py:132-151, stencil.py:115-138,
+ *      blocklinalg.py:50-87).  One object per block shape; built once,
+ *      outside any timed region.  line: extent (nx,1,1); plane: (nx,ny,1). */
+int psm_factors_create(int kind, const psm_stencil* st, int nx, int ny, psm_factors** out);
+int psm_factors_destroy(psm_factors* fac);
+/* Apply the exact block inverse to `count` contiguous blocks of r (device),
+ * writing x (device): the block_update matvec of blocklinalg.py:90-105
+ * without the damping.  Used for API-level checks of the inverse. */
+int psm_factors_apply(const psm_factors* fac, const double* r, double* x, long long count, void* stream);
+
+/* ---- plans (replaces smoother._Plan, smoother.py:112-124, plus the Level's
+ *      adjacency for ghost exchange, grid.py:468-520).  fac[p] is the
+ *      factor object for patch p (NULL entries allowed for ghost-only plans). */
+int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_desc* copies, int ncopy,
+                    const psm_stencil* st, int kind, psm_factors* const* fac, psm_plan** out);
+int psm_plan_destroy(psm_plan* plan);
+/* Number of history slots the plan can hold (grown on demand by the calls below). */
+int psm_plan_reserve_history(psm_plan* plan, int slots);
+
+/* Level.refresh_ghosts (grid.py:507-517): physical ghosts (grid.py:311-330,
+ * ghost = -interior, x then y then z) then interface copies from a snapshot
+ * (grid.py:523-547).  active[p] selects the buffer holding u for patch p.
+ * `what` ORs psm_ghost_part bits: PSM_GHOST_PHYSICAL alone is
+ * fill_physical_ghosts, PSM_GHOST_INTERFACE alone exchange_interface_ghosts;
+ * PSM_GHOST_SKIP_X leaves the physical x faces to the preceding Jacobi sweep,
+ * which already wrote them (fused into its epilogue). */
+enum psm_ghost_part { PSM_GHOST_PHYSICAL = 1, PSM_GHOST_INTERFACE = 2, PSM_GHOST_SKIP_X = 4, PSM_GHOST_ALL = 3 };
+int psm_refresh_ghosts(psm_plan* plan, const unsigned char* active, int what, void* stream);
+
+/* residual_norm partials (smoother.py:96-109): writes the per-plane sums of
+ * (f - A u)^2 of every patch into history slot `slot`. */
+int psm_residual(psm_plan* plan, const unsigned char* active, int slot, void* stream);
+
+/* One block Jacobi sweep (smoother.py:138-153 without the swap/refresh):
+ * v = u + omega * Ainv (f - A u) into the inactive buffer for every line or
+ * plane block of every patch; the residual's squared norm (the history entry
+ * of the current iterate) goes to slot `slot` (slot < 0: not recorded). */
+int psm_jacobi_sweep(psm_plan* plan, const unsigned char* active, double omega, int slot, void* stream);
+
+/* One block Gauss-Seidel sweep in place (smoother.py:156-169, ghosts lagged).
+ * mode PSM_GS_WAVEFRONT reproduces the serial lexicographic order exactly;
+ * PSM_GS_CHAOTIC runs lines without ordering guarantees. */
+int psm_gs_sweep(psm_plan* plan, const unsigned char* active, double omega, int mode, void* stream);
+
+/* Reduce history slots [0, nslots) on the device in a fixed order and copy
+ * the per-slot sums of squares (not square-rooted) to host memory. */
+int psm_history_sumsq(psm_plan* plan, int nslots, double* out_host, void* stream);
+/* Per-plane partial sums of one slot (length = sum of nz over patches), on
+ * the device, for cross-GPU gathers: copied into out_dev. */
+int psm_history_planes(psm_plan* plan, int slot, double* out_dev, void* stream);
+/* Fixed-order (pairwise tree) sum of n doubles on the device -> out_dev[0]. */
+int psm_tree_sum(const double* in_dev, long long n, double* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSMOOTH_H */

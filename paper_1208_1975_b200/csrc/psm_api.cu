@@ -1,0 +1,579 @@
+// C ABI of libpsmooth: factor tables, plans, and the stream-ordered entry
+// points declared in include/psmooth.h.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "psm_internal.cuh"
+
+namespace psm {
+cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
+                              const StencilDev& st, double omega, double* partials, double* rbuf, long long ntiles,
+                              int threads, size_t smem, cudaStream_t stream);
+cudaError_t launch_line_generic(int solve, const PatchDev* patches, int npatch, const unsigned char* active,
+                                const StencilDev& st, double omega, double* partials, long long ntiles,
+                                cudaStream_t stream);
+cudaError_t launch_line_apply(const LineFac* L, const double* r, double* x, long long count, cudaStream_t stream);
+cudaError_t line_tile_kernel_setup(size_t smem);
+cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
+                                   const long long* gprefix, long long total, int skip_x, cudaStream_t stream);
+cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
+                                    int ncopy, long long total, cudaStream_t stream);
+cudaError_t launch_plane_sums(const PatchDev* patches, int npatch, const double* partials, double* plane_sums,
+                              int nplanes, cudaStream_t stream);
+cudaError_t launch_tree_sum(const double* in, long long n, double* out, cudaStream_t stream);
+cudaError_t launch_line_gs(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
+                           const StencilDev& st, double omega, int* flags, long long nunits,
+                           const int* unit_patch, const int* unit_plane, int threads, size_t smem, int grid,
+                           cudaStream_t stream);
+cudaError_t line_gs_kernel_setup(size_t smem);
+int gs_chunks_for(int max_nx);
+size_t gs_smem_per_warp(int nc);
+int gs_occupancy(int nc, int threads, size_t smem);
+cudaError_t launch_line_gs_generic(const PatchDev* patches, int npatch, const unsigned char* active,
+                                   const StencilDev& st, double omega, int wave, long long nlines,
+                                   cudaStream_t stream);
+}  // namespace psm
+
+using namespace psm;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) return fail(PSM_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+// plane path (psm_plane.cu), C++ linkage
+int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F);  // psm_plane.cu
+int psm_plane_apply(const psm_factors* F, const double* r, double* x, long long count, cudaStream_t stream);
+int psm_plane_plan_setup(psm_plan* plan);  // psm_plane.cu
+int psm_plane_plan_free(psm_plan* plan);
+int psm_plane_jacobi(psm_plan* P, const unsigned char* d_active, double omega, double* partials, cudaStream_t s);
+int psm_plane_gs(psm_plan* P, const unsigned char* d_active, double omega, cudaStream_t s);
+
+int psm_set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+extern "C" {
+
+const char* psm_last_error(void) { return g_err.c_str(); }
+int psm_version(void) { return 10000; }
+
+// ---------------------------------------------------------------------------
+// factors
+// ---------------------------------------------------------------------------
+// Tridiagonal tools in long double (80-bit on x86) so the tables are
+// correctly rounded to fp64 in practice.
+static void thomas_ld(int n, long double c, long double lo, long double up, const long double* rhs, long double* x) {
+  std::vector<long double> cp(n), d(n);
+  long double prevc = 0, prevd = 0;
+  for (int i = 0; i < n; ++i) {
+    long double m = c - lo * prevc;
+    cp[i] = up / m;
+    d[i] = (rhs[i] - lo * prevd) / m;
+    prevc = cp[i];
+    prevd = d[i];
+  }
+  x[n - 1] = d[n - 1];
+  for (int i = n - 2; i >= 0; --i) x[i] = d[i] - cp[i] * x[i + 1];
+}
+
+static int build_line(const psm_stencil* st, int nx, psm_factors* F) {
+  const long double c = st->center, lo = st->faces[0], up = st->faces[1];
+  if (fabsl(lo) + fabsl(up) > c)
+    return fail(PSM_ESINGULAR,
+                "line block operator is not diagonally dominant (|%g|+|%g| > %g); the device Thomas solve "
+                "requires dominance",
+                (double)lo, (double)up, (double)c);
+  LineFac& L = F->h_line;
+  memset(&L, 0, sizeof L);
+  std::vector<double> cpN(nx), invmN(nx);
+  long double prev = 0;
+  const long double scale = c + fabsl(lo) + fabsl(up);
+  for (int i = 0; i < nx; ++i) {
+    long double m = c - lo * prev;
+    if (fabsl(m) < 1e-14L * scale) return fail(PSM_ESINGULAR, "pivot %g at %d below 1e-14*|A|", (double)m, i);
+    invmN[i] = (double)(1.0L / m);
+    cpN[i] = (double)(up / m);
+    prev = up / m;
+  }
+  prev = 0;
+  for (int i = 0; i < kSeg; ++i) {
+    long double m = c - lo * prev;
+    L.invm[i] = (double)(1.0L / m);
+    L.cp[i] = (double)(up / m);
+    prev = up / m;
+  }
+  L.lo = (double)lo;
+  L.up = (double)up;
+  L.nx = nx;
+  L.nseg = (nx + kSeg - 1) / kSeg;
+  L.tail = nx - kSeg * (L.nseg - 1);
+  long double e[kSeg], z[kSeg];
+  long double g[kSeg], h[kSeg], gT[kSeg];
+  for (int i = 0; i < kSeg; ++i) e[i] = 0;
+  e[0] = 1;
+  thomas_ld(kSeg, c, lo, up, e, g);
+  e[0] = 0;
+  e[kSeg - 1] = 1;
+  thomas_ld(kSeg, c, lo, up, e, h);
+  for (int i = 0; i < kSeg; ++i) { e[i] = 0; gT[i] = 0; }
+  e[0] = 1;
+  thomas_ld(L.tail, c, lo, up, e, z);
+  for (int i = 0; i < L.tail; ++i) gT[i] = z[i];
+  for (int i = 0; i < kSeg; ++i) {
+    L.g[i] = (double)g[i];
+    L.h[i] = (double)h[i];
+    L.gT[i] = (double)gT[i];
+  }
+  L.up_h31 = (double)(up * h[kSeg - 1]);
+  L.lo_g0 = (double)(lo * g[0]);
+  L.lo_gT0 = (double)(lo * gT[0]);
+  L.d_full = (double)(1.0L / (1.0L - up * lo * h[kSeg - 1] * g[0]));
+  L.d_tail = (double)(1.0L / (1.0L - up * lo * h[kSeg - 1] * gT[0]));
+  // couplings dropped by the 2x2 interface systems
+  const long double dropped = fabsl(lo * g[kSeg - 1]) + fabsl(up * h[0]);
+  L.partitioned = (L.nseg == 1) || (dropped < 1e-18L);
+  const size_t bytes = sizeof(LineFac) + 2 * (size_t)nx * sizeof(double);
+  if (cudaMalloc(&F->dev, bytes) != cudaSuccess) return fail(PSM_ENOMEM, "cudaMalloc(%zu) for line factors", bytes);
+  double* tab = (double*)((char*)F->dev + sizeof(LineFac));
+  L.cpN = tab;
+  L.invmN = tab + nx;
+  F->d_line = (LineFac*)F->dev;
+  CUDA_TRY(cudaMemcpy(F->dev, &L, sizeof L, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(tab, cpN.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(tab + nx, invmN.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
+  return PSM_OK;
+}
+
+
+int psm_factors_create(int kind, const psm_stencil* st, int nx, int ny, psm_factors** out) {
+  if (!st || !out) return fail(PSM_EINVAL, "null argument");
+  *out = nullptr;
+  if (!(st->center > 0) || !isfinite(st->center)) return fail(PSM_EINVAL, "center must be positive and finite");
+  for (int i = 0; i < 6; ++i)
+    if (!isfinite(st->faces[i])) return fail(PSM_EINVAL, "face coefficients must be finite");
+  if (nx < 1 || ny < 1) return fail(PSM_EINVAL, "block extent must be positive, got (%d,%d)", nx, ny);
+  psm_factors* F = new psm_factors();
+  memset(F, 0, sizeof *F);
+  F->kind = kind;
+  F->nx = nx;
+  F->ny = ny;
+  F->center = st->center;
+  memcpy(F->faces, st->faces, sizeof F->faces);
+  int rc;
+  if (kind == PSM_BLOCK_LINE) {
+    rc = build_line(st, nx, F);
+  } else if (kind == PSM_BLOCK_PLANE) {
+    rc = psm_plane_build(st, nx, ny, F);
+  } else {
+    rc = fail(PSM_EINVAL, "unknown block kind %d", kind);
+  }
+  if (rc != PSM_OK) {
+    if (F->dev) cudaFree(F->dev);
+    delete F;
+    return rc;
+  }
+  *out = F;
+  return PSM_OK;
+}
+
+int psm_factors_destroy(psm_factors* F) {
+  if (!F) return PSM_OK;
+  if (F->dev) cudaFree(F->dev);
+  delete F;
+  return PSM_OK;
+}
+
+
+int psm_factors_apply(const psm_factors* F, const double* r, double* x, long long count, void* stream) {
+  if (!F || !r || !x || count < 0) return fail(PSM_EINVAL, "bad arguments to psm_factors_apply");
+  if (F->kind == PSM_BLOCK_LINE) {
+    CUDA_TRY(launch_line_apply(F->d_line, r, x, count, (cudaStream_t)stream));
+    return PSM_OK;
+  }
+  return psm_plane_apply(F, r, x, count, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+static int largest_divisor_le(int n, int cap) {
+  for (int d = std::min(n, std::max(1, cap)); d >= 1; --d)
+    if (n % d == 0) return d;
+  return 1;
+}
+
+
+int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_desc* copies, int ncopy,
+                    const psm_stencil* st, int kind, psm_factors* const* fac, psm_plan** out) {
+  if (!out) return fail(PSM_EINVAL, "null out");
+  *out = nullptr;
+  if (!patches || npatch < 1) return fail(PSM_EINVAL, "a plan needs at least one patch");
+  if (ncopy < 0 || (ncopy > 0 && !copies)) return fail(PSM_EINVAL, "bad interface copy list");
+  if (!st) return fail(PSM_EINVAL, "null stencil");
+  if (kind != 0 && kind != PSM_BLOCK_LINE && kind != PSM_BLOCK_PLANE) return fail(PSM_EINVAL, "bad kind %d", kind);
+  psm_plan* P = new psm_plan();
+  P->npatch = npatch;
+  P->ncopy = ncopy;
+  P->kind = kind;
+  P->st = StencilDev{st->center, st->faces[0], st->faces[1], st->faces[2], st->faces[3], st->faces[4], st->faces[5]};
+  P->hp.resize(npatch);
+  P->fac.assign(npatch, nullptr);
+  int max_nx = 0;
+  for (int p = 0; p < npatch; ++p) {
+    const psm_patch_desc& d = patches[p];
+    if (d.nx < 1 || d.ny < 1 || d.nz < 1) { delete P; return fail(PSM_EINVAL, "patch %d has bad dims", p); }
+    if (!d.buf[0] || !d.buf[1] || !d.f) { delete P; return fail(PSM_EINVAL, "patch %d has null buffers", p); }
+    max_nx = std::max(max_nx, d.nx);
+    if (kind != 0) {
+      psm_factors* F = fac ? fac[p] : nullptr;
+      if (!F || F->kind != kind) { delete P; return fail(PSM_EINVAL, "patch %d lacks matching factors", p); }
+      if (F->nx != d.nx || (kind == PSM_BLOCK_PLANE && F->ny != d.ny)) {
+        delete P;
+        return fail(PSM_EINVAL, "patch %d factors are for another block shape", p);
+      }
+      if (F->center != st->center || memcmp(F->faces, st->faces, sizeof F->faces) != 0) {
+        delete P;
+        return fail(PSM_EINVAL, "patch %d factors were built for another stencil", p);
+      }
+      P->fac[p] = F;
+      if (kind == PSM_BLOCK_LINE && !F->h_line.partitioned) P->tiled = 0;
+    }
+  }
+  if (max_nx > 2048) P->tiled = 0;
+  P->threads = 256;
+  long long tile0 = 0, cell0 = 0;
+  int plane0 = 0;
+  long long g0 = 0;
+  size_t smem = 0;
+  std::vector<long long> gpre(npatch);
+  for (int p = 0; p < npatch; ++p) {
+    const psm_patch_desc& d = patches[p];
+    PatchDev& h = P->hp[p];
+    h.buf[0] = d.buf[0];
+    h.buf[1] = d.buf[1];
+    h.f = d.f;
+    h.nx = d.nx;
+    h.ny = d.ny;
+    h.nz = d.nz;
+    h.R = P->tiled ? largest_divisor_le(d.ny, std::max(1, kMaxTileCells / d.nx)) : 1;
+    h.tiles = (d.ny / h.R) * d.nz;
+    h.tile0 = tile0;
+    h.plane0 = plane0;
+    h.lf = (kind == PSM_BLOCK_LINE) ? P->fac[p]->d_line : nullptr;
+    h.pf = (kind == PSM_BLOCK_PLANE) ? P->fac[p]->d_plane : nullptr;
+    h.cell0 = cell0;
+    cell0 += (long long)d.nx * d.ny * d.nz;
+    tile0 += h.tiles;
+    plane0 += d.nz;
+    gpre[p] = g0;
+    const long long px = d.nx + 2, py = d.ny + 2, pz = d.nz + 2;
+    g0 += 2 * (py * pz + px * pz + px * py);
+    const int nseg = (d.nx + kSeg - 1) / kSeg;
+    smem = std::max(smem, (size_t)(h.R * row_stride(d.nx) + 2 * h.R * nseg) * sizeof(double));
+  }
+  P->ntiles = tile0;
+  P->nplanes = plane0;
+  P->ghost_total = g0;
+  P->smem = smem;
+  std::vector<CopyDev> hc(ncopy);
+  long long e0 = 0;
+  for (int i = 0; i < ncopy; ++i) {
+    const psm_copy_desc& c = copies[i];
+    if (c.src < 0 || c.src >= npatch || c.dst < 0 || c.dst >= npatch || c.src == c.dst) {
+      delete P;
+      return fail(PSM_EINVAL, "copy %d references bad patches", i);
+    }
+    const int sd[3] = {patches[c.src].nx, patches[c.src].ny, patches[c.src].nz};
+    const int dd[3] = {patches[c.dst].nx, patches[c.dst].ny, patches[c.dst].nz};
+    for (int a = 0; a < 3; ++a) {
+      if (c.extent[a] < 1 || c.src_lo[a] < 0 || c.src_lo[a] + c.extent[a] > sd[a] || c.dst_lo[a] < -1 ||
+          c.dst_lo[a] + c.extent[a] > dd[a] + 1) {
+        delete P;
+        return fail(PSM_EINVAL, "copy %d leaves its patches", i);
+      }
+    }
+    CopyDev& h = hc[i];
+    h.src = c.src;
+    h.dst = c.dst;
+    for (int a = 0; a < 3; ++a) {
+      h.src_lo[a] = c.src_lo[a];
+      h.dst_lo[a] = c.dst_lo[a];
+      h.ext[a] = c.extent[a];
+    }
+    h.elem0 = e0;
+    e0 += (long long)c.extent[0] * c.extent[1] * c.extent[2];
+  }
+  P->copy_total = e0;
+  cudaError_t err = cudaMalloc(&P->d_patches, npatch * sizeof(PatchDev));
+  if (err == cudaSuccess) err = cudaMemcpy(P->d_patches, P->hp.data(), npatch * sizeof(PatchDev), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMalloc(&P->d_gprefix, npatch * sizeof(long long));
+  if (err == cudaSuccess) err = cudaMemcpy(P->d_gprefix, gpre.data(), npatch * sizeof(long long), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess && ncopy > 0) {
+    err = cudaMalloc(&P->d_copies, ncopy * sizeof(CopyDev));
+    if (err == cudaSuccess) err = cudaMemcpy(P->d_copies, hc.data(), ncopy * sizeof(CopyDev), cudaMemcpyHostToDevice);
+  }
+  if (err == cudaSuccess) err = cudaMalloc(&P->d_scratch, std::max<long long>(1, P->ntiles) * sizeof(double));
+  if (err == cudaSuccess && kind == PSM_BLOCK_LINE && P->tiled) err = line_tile_kernel_setup(P->smem);
+  if (err != cudaSuccess) {
+    psm_plan_destroy(P);
+    return fail(PSM_ECUDA, "plan setup: %s", cudaGetErrorString(err));
+  }
+  if (kind == PSM_BLOCK_PLANE) {
+    int rc = psm_plane_plan_setup(P);
+    if (rc != PSM_OK) {
+      psm_plan_destroy(P);
+      return rc;
+    }
+  }
+  *out = P;
+  return PSM_OK;
+}
+
+int psm_plan_destroy(psm_plan* P) {
+  if (!P) return PSM_OK;
+  cudaFree(P->d_patches);
+  cudaFree(P->d_copies);
+  cudaFree(P->d_gprefix);
+  cudaFree(P->d_partials);
+  cudaFree(P->d_plane_sums);
+  cudaFree(P->d_sums);
+  cudaFree(P->d_scratch);
+  cudaFree(P->d_flags);
+  cudaFree(P->d_unit_patch);
+  cudaFree(P->d_unit_plane);
+  for (auto& kv : P->active_cache) cudaFree(kv.second);
+  if (P->kind == PSM_BLOCK_PLANE) psm_plane_plan_free(P);
+  delete P;
+  return PSM_OK;
+}
+
+int psm_plan_reserve_history(psm_plan* P, int slots) {
+  if (!P || slots < 0) return fail(PSM_EINVAL, "bad arguments");
+  if (slots <= P->cap_slots) return PSM_OK;
+  int cap = std::max(slots, 2 * P->cap_slots);
+  double *np = nullptr, *ns = nullptr, *nt = nullptr;
+  const size_t tb = (size_t)std::max<long long>(1, P->ntiles) * sizeof(double);
+  const size_t pb = (size_t)std::max(1, P->nplanes) * sizeof(double);
+  if (cudaMalloc(&np, cap * tb) != cudaSuccess || cudaMalloc(&ns, cap * pb) != cudaSuccess ||
+      cudaMalloc(&nt, cap * sizeof(double)) != cudaSuccess) {
+    cudaFree(np);
+    cudaFree(ns);
+    cudaFree(nt);
+    return fail(PSM_ENOMEM, "history workspace for %d slots", cap);
+  }
+  if (P->cap_slots > 0) {
+    CUDA_TRY(cudaMemcpy(np, P->d_partials, P->cap_slots * tb, cudaMemcpyDeviceToDevice));
+  }
+  cudaFree(P->d_partials);
+  cudaFree(P->d_plane_sums);
+  cudaFree(P->d_sums);
+  P->d_partials = np;
+  P->d_plane_sums = ns;
+  P->d_sums = nt;
+  P->cap_slots = cap;
+  return PSM_OK;
+}
+
+static int get_active(psm_plan* P, const unsigned char* active, unsigned char** out) {
+  if (!active) return fail(PSM_EINVAL, "null active vector");
+  std::string key((const char*)active, P->npatch);
+  for (char ch : key)
+    if (ch != 0 && ch != 1) return fail(PSM_EINVAL, "active flags must be 0 or 1");
+  auto it = P->active_cache.find(key);
+  if (it != P->active_cache.end()) {
+    *out = it->second;
+    return PSM_OK;
+  }
+  unsigned char* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, P->npatch));
+  CUDA_TRY(cudaMemcpy(d, active, P->npatch, cudaMemcpyHostToDevice));
+  P->active_cache[key] = d;
+  *out = d;
+  return PSM_OK;
+}
+
+static double* slot_ptr(psm_plan* P, int slot, int* rc) {
+  *rc = PSM_OK;
+  if (slot < 0) return P->d_scratch;
+  if (slot >= P->cap_slots) {
+    *rc = fail(PSM_EINVAL, "history slot %d beyond reserved %d", slot, P->cap_slots);
+    return nullptr;
+  }
+  return P->d_partials + (size_t)slot * std::max<long long>(1, P->ntiles);
+}
+
+int psm_refresh_ghosts(psm_plan* P, const unsigned char* active, int what, void* stream) {
+  if (!P) return fail(PSM_EINVAL, "null plan");
+  if (what < 0 || what > 7) return fail(PSM_EINVAL, "bad ghost selection %d", what);
+  unsigned char* da;
+  int rc = get_active(P, active, &da);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (what & PSM_GHOST_PHYSICAL)
+    CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->d_gprefix, P->ghost_total,
+                                    (what & PSM_GHOST_SKIP_X) ? 1 : 0, s));
+  if (what & PSM_GHOST_INTERFACE)
+    CUDA_TRY(launch_interface_copies(P->d_patches, da, P->d_copies, P->ncopy, P->copy_total, s));
+  return PSM_OK;
+}
+
+int psm_residual(psm_plan* P, const unsigned char* active, int slot, void* stream) {
+  if (!P) return fail(PSM_EINVAL, "null plan");
+  unsigned char* da;
+  int rc = get_active(P, active, &da);
+  if (rc) return rc;
+  double* part = slot_ptr(P, slot, &rc);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (P->tiled) {
+    CUDA_TRY(launch_line_tiles(0, P->d_patches, P->npatch, da, P->st, 0.0, part, nullptr, P->ntiles, P->threads, 0, s));
+  } else {
+    CUDA_TRY(launch_line_generic(0, P->d_patches, P->npatch, da, P->st, 0.0, part, P->ntiles, s));
+  }
+  return PSM_OK;
+}
+
+
+int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int slot, void* stream) {
+  if (!P) return fail(PSM_EINVAL, "null plan");
+  if (!(omega > 0.0 && omega <= 1.0)) return fail(PSM_EINVAL, "omega must lie in (0, 1], got %g", omega);
+  unsigned char* da;
+  int rc = get_active(P, active, &da);
+  if (rc) return rc;
+  double* part = slot_ptr(P, slot, &rc);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (P->kind == PSM_BLOCK_LINE) {
+    if (P->tiled) {
+      CUDA_TRY(launch_line_tiles(1, P->d_patches, P->npatch, da, P->st, omega, part, nullptr, P->ntiles, P->threads,
+                                 P->smem, s));
+    } else {
+      CUDA_TRY(launch_line_generic(1, P->d_patches, P->npatch, da, P->st, omega, part, P->ntiles, s));
+    }
+    return PSM_OK;
+  }
+  if (P->kind == PSM_BLOCK_PLANE) return psm_plane_jacobi(P, da, omega, part, s);
+  return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
+}
+
+
+// Work units (patch, plane) in dependency order and the progress flags of
+// the pipelined line GS kernel; built on first use.
+static int psm_line_gs_prepare(psm_plan* P) {
+  if (P->d_flags) return PSM_OK;
+  int max_nx = 0;
+  for (auto& h : P->hp) max_nx = std::max(max_nx, h.nx);
+  const int nc = gs_chunks_for(max_nx);
+  if (nc == 0) return fail(PSM_EUNSUPPORTED, "pipelined line GS needs nx <= 256");
+  std::vector<int> up, uk;
+  for (int p = 0; p < P->npatch; ++p)
+    for (int k = 0; k < P->hp[p].nz; ++k) {
+      up.push_back(p);
+      uk.push_back(k);
+    }
+  P->nunits = (long long)up.size();
+  CUDA_TRY(cudaMalloc(&P->d_flags, (P->nplanes + 1) * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&P->d_unit_patch, up.size() * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&P->d_unit_plane, uk.size() * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(P->d_unit_patch, up.data(), up.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->d_unit_plane, uk.data(), uk.size() * sizeof(int), cudaMemcpyHostToDevice));
+  P->gs_threads = 128;
+  P->gs_smem = 4 * gs_smem_per_warp(nc);
+  int occ = gs_occupancy(nc, P->gs_threads, P->gs_smem);
+  if (occ < 1) occ = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long want = (P->nunits + 3) / 4;
+  long long grid = std::min<long long>((long long)occ * sms, std::max<long long>(1, want));
+  P->gs_grid = (int)((grid << 4) | nc);
+  return PSM_OK;
+}
+
+int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mode, void* stream) {
+  if (!P) return fail(PSM_EINVAL, "null plan");
+  if (!(omega > 0.0 && omega <= 1.0)) return fail(PSM_EINVAL, "omega must lie in (0, 1], got %g", omega);
+  if (mode != PSM_GS_WAVEFRONT && mode != PSM_GS_CHAOTIC) return fail(PSM_EINVAL, "bad GS mode %d", mode);
+  unsigned char* da;
+  int rc = get_active(P, active, &da);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (P->kind == PSM_BLOCK_PLANE) return psm_plane_gs(P, da, omega, s);
+  if (P->kind != PSM_BLOCK_LINE) return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
+  int max_nx = 0;
+  for (auto& h : P->hp) max_nx = std::max(max_nx, h.nx);
+  if (!P->tiled || gs_chunks_for(max_nx) == 0) {
+    // generic path: one launch per wavefront d = j + k (all patches at once)
+    int maxd = 0;
+    long long nj = 0;
+    for (auto& h : P->hp) {
+      maxd = std::max(maxd, h.ny + h.nz - 1);
+      nj += h.ny;
+    }
+    for (int d = 0; d < maxd; ++d)
+      CUDA_TRY(launch_line_gs_generic(P->d_patches, P->npatch, da, P->st, omega, d, nj, s));
+    return PSM_OK;
+  }
+  rc = psm_line_gs_prepare(P);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemsetAsync(P->d_flags, 0, (P->nplanes + 1) * sizeof(int), s));
+  CUDA_TRY(launch_line_gs(mode, P->d_patches, P->npatch, da, P->st, omega, P->d_flags + 1, P->nunits,
+                          P->d_unit_patch, P->d_unit_plane, P->gs_threads, P->gs_smem, P->gs_grid, s));
+  return PSM_OK;
+}
+
+int psm_history_sumsq(psm_plan* P, int nslots, double* out_host, void* stream) {
+  if (!P || nslots < 0 || (nslots > 0 && !out_host)) return fail(PSM_EINVAL, "bad arguments");
+  if (nslots > P->cap_slots) return fail(PSM_EINVAL, "only %d history slots reserved", P->cap_slots);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t tstride = std::max<long long>(1, P->ntiles);
+  for (int k = 0; k < nslots; ++k) {
+    double* ps = P->d_plane_sums + (size_t)k * std::max(1, P->nplanes);
+    CUDA_TRY(launch_plane_sums(P->d_patches, P->npatch, P->d_partials + k * tstride, ps, P->nplanes, s));
+    CUDA_TRY(launch_tree_sum(ps, P->nplanes, P->d_sums + k, s));
+  }
+  if (nslots > 0) {
+    CUDA_TRY(cudaMemcpyAsync(out_host, P->d_sums, nslots * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  return PSM_OK;
+}
+
+int psm_history_planes(psm_plan* P, int slot, double* out_dev, void* stream) {
+  if (!P || !out_dev) return fail(PSM_EINVAL, "bad arguments");
+  if (slot < 0 || slot >= P->cap_slots) return fail(PSM_EINVAL, "bad slot %d", slot);
+  const size_t tstride = std::max<long long>(1, P->ntiles);
+  CUDA_TRY(launch_plane_sums(P->d_patches, P->npatch, P->d_partials + slot * tstride, out_dev, P->nplanes,
+                             (cudaStream_t)stream));
+  return PSM_OK;
+}
+
+int psm_tree_sum(const double* in_dev, long long n, double* out_dev, void* stream) {
+  if (!in_dev || !out_dev || n < 0) return fail(PSM_EINVAL, "bad arguments");
+  CUDA_TRY(launch_tree_sum(in_dev, n, out_dev, (cudaStream_t)stream));
+  return PSM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// Internal device-side data structures of libpsmooth (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/psmooth.h"
+
+namespace psm {
+
+constexpr int kSeg = 32;  // line segment owned by one solver lane
+
+// Exact line-block inverse in partitioned form (built by psm_factors_create).
+// The closure-free line operator tridiag(lo, c, up) of order nx
+// (stencil.py:115-138 with extent (nx,1,1)) is split into segments of 32
+// (the last one `tail` long).  Every segment is the same local block, so one
+// set of Thomas factors and two spike columns serves all of them:
+//   g = T_32^{-1} e_0, h = T_32^{-1} e_31, gT = T_tail^{-1} e_0.
+// A segment's exact solution is y - lo*x_left*g - up*x_right*h where y solves
+// the local block; the interface values follow from 2x2 systems whose
+// couplings to farther segments are below lo*g[31], up*h[0] (checked < 1e-18
+// at build time, else the plan uses the generic full-Thomas kernel).
+struct LineFac {
+  double cp[kSeg], invm[kSeg];  // Thomas factors (prefix-valid for the tail)
+  double g[kSeg], h[kSeg];      // spikes of a full segment
+  double gT[kSeg];              // left spike of the tail segment
+  double lo, up;                // coefficient of x-1 and x+1
+  double up_h31;                // up * h[31]
+  double lo_g0, lo_gT0;         // lo * g[0], lo * gT[0]
+  double d_full, d_tail;        // 1/(1 - up*lo*h31*g0), same with gT0
+  int nx, nseg, tail;
+  int partitioned;              // 1: segment kernel valid; 0: generic kernel
+  // generic full-length Thomas factors (device pointers into the same
+  // allocation), used when partitioned == 0
+  const double* cpN;
+  const double* invmN;
+};
+
+// Exact plane-block inverse: DST-I along x, then one tridiagonal system in y
+// per x-mode (diagonal center + 2*a*cos(pi i/(nx+1))).
+struct PlaneFac {
+  int nx, ny;
+  double fy_lo, fy_up;
+  const double* Q;     // nx*nx orthonormal DST-I basis, symmetric
+  const double* cp;    // [mode][ny] Thomas factors
+  const double* invm;  // [mode][ny]
+};
+
+struct PatchDev {
+  double* buf[2];
+  const double* f;
+  int nx, ny, nz;
+  int R;          // rows (x-lines) per tile, divides ny
+  int tiles;      // ny*nz/R
+  long long tile0;  // first global tile
+  int plane0;     // first global plane (prefix of nz)
+  long long cell0;  // first interior cell (prefix of nx*ny*nz), for plane workspaces
+  const LineFac* lf;
+  const PlaneFac* pf;
+};
+
+struct CopyDev {
+  int src, dst;
+  int src_lo[3], dst_lo[3], ext[3];
+  long long elem0;  // prefix of element counts
+};
+
+struct StencilDev {
+  double c, xm, xp, ym, yp, zm, zp;
+};
+
+__host__ __device__ inline int row_stride(int nx) { return nx + (nx + kSeg - 1) / kSeg; }
+
+__device__ __forceinline__ int find_patch(const PatchDev* __restrict__ p, int n, long long tile) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// reference residual order (stencil.py:106-111): acc = c*u; acc += face*nbr
+// for -x,+x,-y,+y,-z,+z; r = f - acc.  No FMA contraction, so the value is
+// bit-identical to the reference for the same u and f.
+__device__ __forceinline__ double residual7(const StencilDev& s, double f, double c, double xm, double xp,
+                                            double ym, double yp, double zm, double zp) {
+  double acc = __dmul_rn(s.c, c);
+  acc = __dadd_rn(acc, __dmul_rn(s.xm, xm));
+  acc = __dadd_rn(acc, __dmul_rn(s.xp, xp));
+  acc = __dadd_rn(acc, __dmul_rn(s.ym, ym));
+  acc = __dadd_rn(acc, __dmul_rn(s.yp, yp));
+  acc = __dadd_rn(acc, __dmul_rn(s.zm, zm));
+  acc = __dadd_rn(acc, __dmul_rn(s.zp, zp));
+  return __dsub_rn(f, acc);
+}
+
+// block_update (smoother.py:93): u + omega * x, two roundings like numpy
+__device__ __forceinline__ double relax(double u, double omega, double x) {
+  return __dadd_rn(u, __dmul_rn(omega, x));
+}
+
+constexpr int kMaxTileCells = 2048;  // cells per line tile (8 per thread at 256 threads)
+
+}  // namespace psm
+
+#include <map>
+#include <string>
+#include <vector>
+
+struct PlaneState;  // psm_plane.cu
+
+struct psm_factors {
+  // host handle for one block shape
+  int kind;
+  int nx, ny;
+  void* dev;            // one allocation: struct + tables
+  psm::LineFac* d_line;      // kind == line
+  psm::PlaneFac* d_plane;    // kind == plane
+  psm::LineFac h_line;       // host copy (pointers refer to device memory)
+  psm::PlaneFac h_plane;
+  double center, faces[6];
+};
+
+struct psm_plan {
+  int npatch = 0, ncopy = 0, kind = 0;
+  psm::StencilDev st{};
+  std::vector<psm::PatchDev> hp;
+  std::vector<psm_factors*> fac;
+  psm::PatchDev* d_patches = nullptr;
+  psm::CopyDev* d_copies = nullptr;
+  long long copy_total = 0;
+  long long* d_gprefix = nullptr;
+  long long ghost_total = 0;
+  long long ntiles = 0;
+  int nplanes = 0;
+  int threads = 256;
+  size_t smem = 0;
+  int tiled = 1;  // line tile kernel usable (else generic one-thread-per-line kernels)
+  std::map<std::string, unsigned char*> active_cache;
+  int cap_slots = 0;
+  double* d_partials = nullptr;    // cap_slots * ntiles
+  double* d_plane_sums = nullptr;  // cap_slots * nplanes
+  double* d_sums = nullptr;        // cap_slots
+  double* d_scratch = nullptr;     // ntiles, for unrecorded sweeps
+  // line GS
+  int* d_flags = nullptr;         // per (patch, plane) progress counters
+  int* d_unit_patch = nullptr;    // GS work units (patch, plane) in dependency order
+  int* d_unit_plane = nullptr;
+  long long nunits = 0;
+  int gs_threads = 0, gs_grid = 0;
+  size_t gs_smem = 0;
+  int sweep_count = 0;
+  // plane path
+  PlaneState* plane = nullptr;
+};
+

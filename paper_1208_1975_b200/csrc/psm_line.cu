@@ -1,0 +1,274 @@
+// Line-block (x-line) kernels: block Jacobi sweep, residual norm, and the
+// generic full-Thomas fallback.
+//
+// Replaces, for block_dims (>=nx, 1, 1):
+//   smoother._jacobi_step + work()        smoother.py:138-153
+//   stencil.block_residual                 stencil.py:93-112
+//   smoother.block_update -> matvec        smoother.py:90-93, blocklinalg.py:90-105
+//   smoother.residual_norm (partials)      smoother.py:96-109
+//
+// Tile kernel structure (one CTA = R consecutive x-lines of one z-plane):
+//   A  coalesced: r = f - A u for every cell (reference operation order),
+//      x-neighbours by warp shuffle, y/z-neighbours straight from L2; r goes
+//      to shared memory (one pad double per 32 so segment reads are
+//      conflict-free) and r^2 into the tile's norm partial.
+//   B  one lane per 32-cell segment: Thomas on the segment with constant
+//      factors, result y back to smem, segment end values to an exchange row.
+//   C  coalesced: interface 2x2 solves (redundantly per cell, broadcast smem
+//      reads), spike correction, v = u + omega*x, store v and the physical
+//      x-face ghosts of v (grid.py:321-322 rule, fused).
+#include "psm_internal.cuh"
+
+namespace psm {
+
+constexpr int kMaxE = 8;  // cells per thread per tile
+
+template <int MODE>  // 0: residual partials only, 1: Jacobi sweep, 2: residual to rbuf (plane path)
+__global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                                        const unsigned char* __restrict__ active, StencilDev st,
+                                                        double omega, double* __restrict__ partials,
+                                                        double* __restrict__ rbuf) {
+  extern __shared__ double sm[];
+  __shared__ double wsum[32];
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
+  const long long tile = blockIdx.x;
+  const int pi = find_patch(patches, npatch, tile);
+  const PatchDev& P = patches[pi];
+  const int nx = P.nx, ny = P.ny, R = P.R;
+  const long long cell0 = P.cell0;
+  const LineFac* __restrict__ L = P.lf;
+  const int row0 = (int)(tile - P.tile0) * R;
+  const int k = row0 / ny, j0 = row0 - k * ny;
+  const long long px = nx + 2, pxy = px * (ny + 2);
+  const int act = active[pi];
+  const double* __restrict__ u = P.buf[act];
+  double* __restrict__ v = P.buf[act ^ 1];
+  const double* __restrict__ f = P.f;
+  const long long ubase = (long long)(k + 1) * pxy + (long long)(j0 + 1) * px + 1;  // u(0, j0, k)
+  const long long fbase = ((long long)k * ny + j0) * nx;
+  const int nelem = R * nx;
+  const int RS = row_stride(nx);
+  double* rs = sm;
+
+  double ssq = 0.0;
+  double ucen[kMaxE];
+#pragma unroll
+  for (int h = 0; h < kMaxE; h += 4) {
+    if (h * T >= nelem) break;
+    double c[4], ym[4], yp[4], zm[4], zp[4], fv[4];
+    int xr[4], rr[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = (h + q) * T + tid;
+      ok[q] = e < nelem;
+      rr[q] = ok[q] ? e / nx : 0;
+      xr[q] = ok[q] ? e - rr[q] * nx : 0;
+      const long long iu = ubase + (long long)rr[q] * px + xr[q];
+      if (ok[q]) {
+        c[q] = __ldg(u + iu);
+        ym[q] = __ldg(u + iu - px);
+        yp[q] = __ldg(u + iu + px);
+        zm[q] = __ldg(u + iu - pxy);
+        zp[q] = __ldg(u + iu + pxy);
+        fv[q] = __ldg(f + fbase + e);
+      } else {
+        c[q] = ym[q] = yp[q] = zm[q] = zp[q] = fv[q] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double xl = __shfl_up_sync(0xffffffffu, c[q], 1);
+      double xp_ = __shfl_down_sync(0xffffffffu, c[q], 1);
+      ucen[h + q] = c[q];
+      if (ok[q]) {
+        const long long iu = ubase + (long long)rr[q] * px + xr[q];
+        if (lane == 0 || xr[q] == 0) xl = __ldg(u + iu - 1);
+        if (lane == 31 || xr[q] == nx - 1) xp_ = __ldg(u + iu + 1);
+        const double res = residual7(st, fv[q], c[q], xl, xp_, ym[q], yp[q], zm[q], zp[q]);
+        ssq = fma(res, res, ssq);
+        if (MODE == 1) rs[rr[q] * RS + xr[q] + (xr[q] >> 5)] = res;
+        if (MODE == 2) rbuf[cell0 + fbase + (h + q) * T + tid] = res;
+      }
+    }
+  }
+  // deterministic tile partial of sum(r^2): fixed shuffle tree, warps in order
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+  if (lane == 0) wsum[tid >> 5] = ssq;
+  __syncthreads();
+  if (tid == 0 && partials) {
+    double s = 0.0;
+    for (int w = 0; w < (T >> 5); ++w) s += wsum[w];
+    partials[tile] = s;
+  }
+  if (MODE != 1) return;
+
+  // ---- B: local segment solves -------------------------------------------
+  const int nseg = L->nseg, tail = L->tail;
+  double* ex = sm + R * RS;
+  const double lo = L->lo;
+  for (int ln = tid; ln < R * nseg; ln += T) {
+    const int r = ln / nseg, s = ln - r * nseg;
+    const int len = (s == nseg - 1) ? tail : kSeg;
+    double* seg = rs + r * RS + s * (kSeg + 1);
+    // forward elimination and back substitution in place in shared memory
+    double prev = 0.0;
+#pragma unroll
+    for (int i = 0; i < kSeg; ++i) {
+      if (i < len) {
+        prev = fma(-lo, prev, seg[i]) * __ldg(&L->invm[i]);
+        seg[i] = prev;
+      }
+    }
+    const double ylast = prev;  // y[len-1] is final after the forward pass
+    double next = prev;
+#pragma unroll
+    for (int i = kSeg - 2; i >= 0; --i) {
+      if (i < len - 1) {
+        next = fma(-__ldg(&L->cp[i]), next, seg[i]);
+        seg[i] = next;
+      }
+    }
+    ex[2 * ln] = next;
+    ex[2 * ln + 1] = ylast;
+  }
+  __syncthreads();
+
+  // ---- C: interfaces, spike correction, relaxation, store ----------------
+  const double up = L->up, up_h31 = L->up_h31;
+#pragma unroll
+  for (int h = 0; h < kMaxE; ++h) {
+    const int e = h * T + tid;
+    if (h * T >= nelem) break;
+    if (e < nelem) {
+      const int r = e / nx, x = e - r * nx;
+      const int s = x >> 5, i = x & (kSeg - 1);
+      const int ln = r * nseg + s;
+      const bool last = (s == nseg - 1);
+      const double y = rs[r * RS + x + s];
+      double cl = 0.0, cr = 0.0;
+      if (s > 0) {
+        const double xl = (ex[2 * ln - 1] - up_h31 * ex[2 * ln]) * (last ? L->d_tail : L->d_full);
+        cl = lo * xl;
+      }
+      if (!last) {
+        const bool rlast = (s + 1 == nseg - 1);
+        const double yfr = ex[2 * ln + 2];
+        const double xl2 = (ex[2 * ln + 1] - up_h31 * yfr) * (rlast ? L->d_tail : L->d_full);
+        const double xf = yfr - (rlast ? L->lo_gT0 : L->lo_g0) * xl2;
+        cr = up * xf;
+      }
+      const double gi = last ? __ldg(&L->gT[i]) : __ldg(&L->g[i]);
+      const double xs = fma(-cr, __ldg(&L->h[i]), fma(-cl, gi, y));
+      const double nv = relax(ucen[h], omega, xs);
+      const long long iu = ubase + (long long)r * px + x;
+      v[iu] = nv;
+      if (x == 0) v[iu - 1] = -nv;
+      if (x == nx - 1) v[iu + 1] = -nv;
+    }
+  }
+}
+
+// Generic exact line sweep: one thread per x-line, full-length Thomas with
+// per-position factors (any nx, any stencil with a nonsingular pivot chain).
+// The forward pass stages y' in v's interior; the backward pass overwrites it
+// with the relaxed value.  Tiles have R = 1 (one line per partial).
+__global__ void line_generic_jacobi_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                           const unsigned char* __restrict__ active, StencilDev st,
+                                           double omega, double* __restrict__ partials, long long ntiles,
+                                           int solve) {
+  const long long tile = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (tile >= ntiles) return;
+  const int pi = find_patch(patches, npatch, tile);
+  const PatchDev& P = patches[pi];
+  const int nx = P.nx, ny = P.ny;
+  const int row = (int)(tile - P.tile0);
+  const int k = row / ny, j = row - k * ny;
+  const long long px = nx + 2, pxy = px * (ny + 2);
+  const int act = active[pi];
+  const double* u = P.buf[act];
+  double* v = P.buf[act ^ 1];
+  const long long ub = (long long)(k + 1) * pxy + (long long)(j + 1) * px + 1;
+  const double* fr = P.f + ((long long)k * ny + j) * nx;
+  const LineFac* L = P.lf;
+  double ssq = 0.0, prev = 0.0;
+  for (int x = 0; x < nx; ++x) {
+    const long long iu = ub + x;
+    const double r = residual7(st, fr[x], u[iu], u[iu - 1], u[iu + 1], u[iu - px], u[iu + px], u[iu - pxy],
+                               u[iu + pxy]);
+    ssq = fma(r, r, ssq);
+    if (solve) {
+      prev = fma(-L->lo, prev, r) * L->invmN[x];
+      v[iu] = prev;
+    }
+  }
+  if (partials) partials[tile] = ssq;
+  if (!solve) return;
+  double next = 0.0;
+  for (int x = nx - 1; x >= 0; --x) {
+    const long long iu = ub + x;
+    const double yx = (x == nx - 1) ? v[iu] : fma(-L->cpN[x], next, v[iu]);
+    next = yx;
+    v[iu] = relax(u[iu], omega, yx);
+  }
+  v[ub - 1] = -v[ub];
+  v[ub + nx] = -v[ub + nx - 1];
+}
+
+// Apply the exact line inverse to `count` contiguous vectors of length nx
+// (psm_factors_apply): one thread per vector, full-length Thomas.
+__global__ void line_apply_kernel(const LineFac* __restrict__ L, const double* __restrict__ r,
+                                  double* __restrict__ x, long long count) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  const int nx = L->nx;
+  const double* rb = r + b * nx;
+  double* xb = x + b * nx;
+  double prev = 0.0;
+  for (int i = 0; i < nx; ++i) {
+    prev = fma(-L->lo, prev, rb[i]) * L->invmN[i];
+    xb[i] = prev;
+  }
+  for (int i = nx - 2; i >= 0; --i) xb[i] = fma(-L->cpN[i], xb[i + 1], xb[i]);
+}
+
+// ---- host-side launchers ---------------------------------------------------
+cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
+                              const StencilDev& st, double omega, double* partials, double* rbuf, long long ntiles,
+                              int threads, size_t smem, cudaStream_t stream) {
+  if (ntiles == 0) return cudaSuccess;
+  if (mode == 0) {
+    line_tile_kernel<0><<<(unsigned)ntiles, threads, 0, stream>>>(patches, npatch, active, st, omega, partials,
+                                                                  nullptr);
+  } else if (mode == 1) {
+    line_tile_kernel<1><<<(unsigned)ntiles, threads, smem, stream>>>(patches, npatch, active, st, omega, partials,
+                                                                     nullptr);
+  } else {
+    line_tile_kernel<2><<<(unsigned)ntiles, threads, 0, stream>>>(patches, npatch, active, st, omega, partials,
+                                                                  rbuf);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_line_generic(int solve, const PatchDev* patches, int npatch, const unsigned char* active,
+                                const StencilDev& st, double omega, double* partials, long long ntiles,
+                                cudaStream_t stream) {
+  if (ntiles == 0) return cudaSuccess;
+  const int tpb = 128;
+  line_generic_jacobi_kernel<<<(unsigned)((ntiles + tpb - 1) / tpb), tpb, 0, stream>>>(
+      patches, npatch, active, st, omega, partials, ntiles, solve);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_line_apply(const LineFac* L, const double* r, double* x, long long count, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  line_apply_kernel<<<(unsigned)((count + 127) / 128), 128, 0, stream>>>(L, r, x, count);
+  return cudaGetLastError();
+}
+
+cudaError_t line_tile_kernel_setup(size_t smem) {
+  return cudaFuncSetAttribute(line_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+}  // namespace psm

@@ -1,0 +1,373 @@
+// Plane-block (xy-plane) kernels: exact plane inverse, Jacobi and GS sweeps.
+//
+// Replaces, for block_dims (>=nx, >=ny, 1):
+//   InverseCache.get -> invert_dense of the (nx*ny)^2 plane operator
+//       blocklinalg.py:132-151, stencil.py:115-138 (infeasible beyond ~48^2:
+//       SURVEY F8), and its dense matvec blocklinalg.py:90-105
+//   smoother._jacobi_step / _gs_step with plane blocks  smoother.py:138-169
+//
+// The closure-free plane operator c*I + a*(S_x (x) I) + (fy-, fy+ couplings
+// in y) with symmetric x faces a = faces[0] = faces[1] is diagonalised along
+// x by the orthonormal DST-I basis Q (Q = Q^T = Q^-1).  Per x-mode i the
+// remaining operator is tridiagonal in y with diagonal c + 2a cos(pi i/(nx+1)).
+// So Ainv r = Q * T_i^-1 * (Q r): a GEMM with Q along x, one Thomas solve
+// along y per (plane, mode), and a GEMM back.  The two transforms are plain
+// dense fp64 GEMMs (cuBLAS DGEMM, tensor-core DMMA on sm_100a); the residual,
+// the modal Thomas solves and the relaxation are this file's kernels.
+#include <cublas_v2.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "psm_internal.cuh"
+
+namespace psm {
+cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
+                              const StencilDev& st, double omega, double* partials, double* rbuf, long long ntiles,
+                              int threads, size_t smem, cudaStream_t stream);
+
+// r = f - A u of every cell of plane `k` of every patch with nz > k (GS
+// stage) into the compact stage buffer, rows of the same patch contiguous.
+__global__ void plane_stage_residual_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                            const unsigned char* __restrict__ active, StencilDev st, int k,
+                                            const long long* __restrict__ stage_off, double* __restrict__ rbuf,
+                                            long long total) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = npatch - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (stage_off[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const PatchDev& P = patches[lo];
+    if (k >= P.nz) continue;
+    const long long e = g - stage_off[lo];
+    const int nx = P.nx, ny = P.ny;
+    if (e >= (long long)nx * ny) continue;
+    const int j = (int)(e / nx), x = (int)(e - (long long)j * nx);
+    const long long px = nx + 2, pxy = px * (ny + 2);
+    const double* u = P.buf[active[lo]];
+    const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
+    rbuf[g] = residual7(st, P.f[((long long)k * ny + j) * nx + x], u[iu], u[iu - 1], u[iu + 1], u[iu - px],
+                        u[iu + px], u[iu - pxy], u[iu + pxy]);
+  }
+}
+
+// Thomas along y for every (plane, mode) of a batch of planes that share one
+// PlaneFac.  Layout: plane-major, then y, then mode (x-mode fastest), so
+// threads of a warp take consecutive modes (coalesced).  In place.
+__global__ void plane_modal_thomas_kernel(const PlaneFac* __restrict__ F, double* __restrict__ buf, long long nplanes) {
+  const int nx = F->nx, ny = F->ny;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= nplanes * nx) return;
+  const long long pl = t / nx;
+  const int i = (int)(t - pl * nx);
+  double* b = buf + pl * (long long)nx * ny + i;
+  const double* cp = F->cp + i;
+  const double* invm = F->invm + i;
+  const double lo = F->fy_lo;
+  double prev = 0.0;
+  for (int j = 0; j < ny; ++j) {
+    prev = fma(-lo, prev, b[(long long)j * nx]) * invm[(long long)j * nx];
+    b[(long long)j * nx] = prev;
+  }
+  double next = prev;
+  for (int j = ny - 2; j >= 0; --j) {
+    next = fma(-cp[(long long)j * nx], next, b[(long long)j * nx]);
+    b[(long long)j * nx] = next;
+  }
+}
+
+// Jacobi epilogue: v = u + omega * x for every interior cell, plus the
+// physical x-face ghosts of v (fused, see psm_line.cu).
+__global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                   const unsigned char* __restrict__ active, double omega,
+                                   const double* __restrict__ xbuf, long long total) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = npatch - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (patches[mid].cell0 <= g) lo = mid; else hi = mid - 1;
+    }
+    const PatchDev& P = patches[lo];
+    const long long e = g - P.cell0;
+    const int nx = P.nx, ny = P.ny;
+    const long long row = e / nx;
+    const int x = (int)(e - row * nx);
+    const int k = (int)(row / ny), j = (int)(row - (long long)k * ny);
+    const long long px = nx + 2, pxy = px * (ny + 2);
+    const int act = active[lo];
+    const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
+    const double nv = relax(P.buf[act][iu], omega, xbuf[g]);
+    double* v = P.buf[act ^ 1];
+    v[iu] = nv;
+    if (x == 0) v[iu - 1] = -nv;
+    if (x == nx - 1) v[iu + 1] = -nv;
+  }
+}
+
+// GS epilogue for stage k: u = u + omega * x in place on plane k.
+__global__ void plane_stage_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                         const unsigned char* __restrict__ active, double omega, int k,
+                                         const long long* __restrict__ stage_off, const double* __restrict__ xbuf,
+                                         long long total) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = npatch - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (stage_off[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const PatchDev& P = patches[lo];
+    if (k >= P.nz) continue;
+    const long long e = g - stage_off[lo];
+    const int nx = P.nx, ny = P.ny;
+    if (e >= (long long)nx * ny) continue;
+    const int j = (int)(e / nx), x = (int)(e - (long long)j * nx);
+    const long long px = nx + 2, pxy = px * (ny + 2);
+    double* u = P.buf[active[lo]];
+    const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
+    u[iu] = relax(u[iu], omega, xbuf[g]);
+  }
+}
+
+static unsigned blocks_for(long long n, int tpb) {
+  long long b = (n + tpb - 1) / tpb;
+  if (b > 148LL * 32) b = 148LL * 32;
+  return (unsigned)std::max<long long>(1, b);
+}
+
+}  // namespace psm
+
+using namespace psm;
+
+// per-plan state of the plane path
+struct PlaneRun {  // consecutive patches sharing one PlaneFac (same nx, ny)
+  int p0, p1;
+  const PlaneFac* d_fac;
+  const double* Q;
+  int nx, ny;
+};
+
+struct PlaneState {
+  cublasHandle_t handle = nullptr;
+  double* rbuf = nullptr;   // sum of cells: residual, then x
+  double* rhat = nullptr;   // sum of cells: modal coefficients
+  double* sbuf = nullptr;   // GS stage buffers (sum over patches of nx*ny), x2
+  double* shat = nullptr;
+  long long* d_stage_off = nullptr;
+  long long stage_total = 0;
+  std::vector<long long> stage_off;
+  std::vector<PlaneRun> runs;
+};
+
+
+// error plumbing shared with psm_api.cu
+int psm_set_error(int code, const char* msg);
+
+#define PCUDA(expr)                                                                      \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(_e));      \
+  } while (0)
+#define PBLAS(expr)                                                                      \
+  do {                                                                                   \
+    cublasStatus_t _s = (expr);                                                          \
+    if (_s != CUBLAS_STATUS_SUCCESS) return psm_set_error(PSM_ECUDA, "cuBLAS call failed: " #expr); \
+  } while (0)
+
+int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
+  const long double c = st->center, a = st->faces[0], b = st->faces[1];
+  const long double ylo = st->faces[2], yup = st->faces[3];
+  if (a != b)
+    return psm_set_error(PSM_EUNSUPPORTED,
+                         "plane blocks need symmetric x faces (faces[0] == faces[1]) for the DST factorisation");
+  if (2 * fabsl(a) + fabsl(ylo) + fabsl(yup) > c)
+    return psm_set_error(PSM_ESINGULAR, "plane block operator is not diagonally dominant");
+  const size_t nq = (size_t)nx * nx, nt = (size_t)nx * ny;
+  std::vector<double> Q(nq), cp(nt), invm(nt);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const long double sc = sqrtl(2.0L / (nx + 1));
+  for (int p = 0; p < nx; ++p)
+    for (int i = 0; i < nx; ++i) Q[(size_t)p * nx + i] = (double)(sc * sinl(pi * (p + 1) * (i + 1) / (nx + 1)));
+  for (int i = 0; i < nx; ++i) {
+    const long double d = c + 2.0L * a * cosl(pi * (i + 1) / (nx + 1));
+    long double prev = 0;
+    for (int j = 0; j < ny; ++j) {
+      const long double m = d - ylo * prev;
+      if (fabsl(m) < 1e-14L * c) return psm_set_error(PSM_ESINGULAR, "plane modal pivot below 1e-14*|A|");
+      invm[(size_t)j * nx + i] = (double)(1.0L / m);
+      cp[(size_t)j * nx + i] = (double)(yup / m);
+      prev = yup / m;
+    }
+  }
+  const size_t bytes = sizeof(PlaneFac) + (nq + 2 * nt) * sizeof(double);
+  if (cudaMalloc(&F->dev, bytes) != cudaSuccess) return psm_set_error(PSM_ENOMEM, "cudaMalloc for plane factors");
+  double* tab = (double*)((char*)F->dev + sizeof(PlaneFac));
+  PlaneFac& H = F->h_plane;
+  memset(&H, 0, sizeof H);
+  H.nx = nx;
+  H.ny = ny;
+  H.fy_lo = (double)ylo;
+  H.fy_up = (double)yup;
+  H.Q = tab;
+  H.cp = tab + nq;
+  H.invm = tab + nq + nt;
+  F->d_plane = (PlaneFac*)F->dev;
+  PCUDA(cudaMemcpy(F->dev, &H, sizeof H, cudaMemcpyHostToDevice));
+  PCUDA(cudaMemcpy(tab, Q.data(), nq * sizeof(double), cudaMemcpyHostToDevice));
+  PCUDA(cudaMemcpy(tab + nq, cp.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  PCUDA(cudaMemcpy(tab + nq + nt, invm.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  return PSM_OK;
+}
+
+// out = Q_x applied to `nvec` row-major vectors of length nx stored with
+// leading dimension nx: in column-major terms out(nx x nvec) = Q * in.
+static int dst_gemm(cublasHandle_t h, const double* Q, int nx, const double* in, double* out, long long nvec) {
+  const double one = 1.0, zero = 0.0;
+  // split huge batches so n fits an int
+  const long long maxn = 1LL << 30;
+  for (long long off = 0; off < nvec; off += maxn) {
+    const int n = (int)std::min(maxn, nvec - off);
+    PBLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, nx, n, nx, &one, Q, nx, in + off * nx, nx, &zero,
+                      out + off * nx, nx));
+  }
+  return PSM_OK;
+}
+
+int psm_plane_apply(const psm_factors* F, const double* r, double* x, long long count, cudaStream_t stream) {
+  if (F->kind != PSM_BLOCK_PLANE) return psm_set_error(PSM_EINVAL, "not a plane factor object");
+  const PlaneFac& H = F->h_plane;
+  const long long n = (long long)H.nx * H.ny * count;
+  if (n == 0) return PSM_OK;
+  double* tmp = nullptr;
+  PCUDA(cudaMallocAsync(&tmp, n * sizeof(double), stream));
+  cublasHandle_t h;
+  PBLAS(cublasCreate(&h));
+  cublasSetStream(h, stream);
+  int rc = dst_gemm(h, H.Q, H.nx, r, tmp, (long long)H.ny * count);
+  if (rc == PSM_OK) {
+    plane_modal_thomas_kernel<<<(unsigned)((count * H.nx + 127) / 128), 128, 0, stream>>>(F->d_plane, tmp, count);
+    rc = dst_gemm(h, H.Q, H.nx, tmp, x, (long long)H.ny * count);
+  }
+  cudaFreeAsync(tmp, stream);
+  cudaStreamSynchronize(stream);
+  cublasDestroy(h);
+  return rc;
+}
+
+int psm_plane_plan_setup(psm_plan* P) {
+  PlaneState* S = new PlaneState();
+  P->plane = S;
+  PBLAS(cublasCreate(&S->handle));
+  long long cells = 0;
+  for (auto& h : P->hp) cells += (long long)h.nx * h.ny * h.nz;
+  PCUDA(cudaMalloc(&S->rbuf, cells * sizeof(double)));
+  PCUDA(cudaMalloc(&S->rhat, cells * sizeof(double)));
+  S->stage_off.resize(P->npatch);
+  long long so = 0;
+  for (int p = 0; p < P->npatch; ++p) {
+    S->stage_off[p] = so;
+    so += (long long)P->hp[p].nx * P->hp[p].ny;
+  }
+  S->stage_total = so;
+  PCUDA(cudaMalloc(&S->sbuf, so * sizeof(double)));
+  PCUDA(cudaMalloc(&S->shat, so * sizeof(double)));
+  PCUDA(cudaMalloc(&S->d_stage_off, P->npatch * sizeof(long long)));
+  PCUDA(cudaMemcpy(S->d_stage_off, S->stage_off.data(), P->npatch * sizeof(long long), cudaMemcpyHostToDevice));
+  for (int p = 0; p < P->npatch;) {
+    int q = p + 1;
+    while (q < P->npatch && P->fac[q] == P->fac[p]) ++q;
+    PlaneRun r;
+    r.p0 = p;
+    r.p1 = q;
+    r.d_fac = P->fac[p]->d_plane;
+    r.Q = P->fac[p]->h_plane.Q;
+    r.nx = P->hp[p].nx;
+    r.ny = P->hp[p].ny;
+    S->runs.push_back(r);
+    p = q;
+  }
+  return PSM_OK;
+}
+
+int psm_plane_plan_free(psm_plan* P) {
+  PlaneState* S = P->plane;
+  if (!S) return PSM_OK;
+  if (S->handle) cublasDestroy(S->handle);
+  cudaFree(S->rbuf);
+  cudaFree(S->rhat);
+  cudaFree(S->sbuf);
+  cudaFree(S->shat);
+  cudaFree(S->d_stage_off);
+  delete S;
+  P->plane = nullptr;
+  return PSM_OK;
+}
+
+// Jacobi: residual of every cell (tile kernel, mode 2 stores r) -> DST ->
+// modal Thomas -> DST back -> relax into v.
+int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double* partials, cudaStream_t s) {
+  PlaneState* S = P->plane;
+  PCUDA(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, S->rbuf, P->ntiles, P->threads, 0,
+                          s));
+  cublasSetStream(S->handle, s);
+  for (const PlaneRun& r : S->runs) {
+    const long long c0 = P->hp[r.p0].cell0;
+    long long planes = 0;
+    for (int p = r.p0; p < r.p1; ++p) planes += P->hp[p].nz;
+    const long long nvec = planes * r.ny;
+    int rc = dst_gemm(S->handle, r.Q, r.nx, S->rbuf + c0, S->rhat + c0, nvec);
+    if (rc) return rc;
+    plane_modal_thomas_kernel<<<(unsigned)((planes * r.nx + 127) / 128), 128, 0, s>>>(r.d_fac, S->rhat + c0, planes);
+    PCUDA(cudaGetLastError());
+    rc = dst_gemm(S->handle, r.Q, r.nx, S->rhat + c0, S->rbuf + c0, nvec);
+    if (rc) return rc;
+  }
+  long long cells = 0;
+  for (auto& h : P->hp) cells += (long long)h.nx * h.ny * h.nz;
+  plane_relax_kernel<<<blocks_for(cells, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega, S->rbuf, cells);
+  PCUDA(cudaGetLastError());
+  return PSM_OK;
+}
+
+// Lexicographic plane GS: planes in k order, all patches of the level at
+// each stage (patches couple only through step-end ghosts).
+int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_t s) {
+  PlaneState* S = P->plane;
+  cublasSetStream(S->handle, s);
+  int maxnz = 0;
+  for (auto& h : P->hp) maxnz = std::max(maxnz, h.nz);
+  for (int k = 0; k < maxnz; ++k) {
+    plane_stage_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(
+        P->d_patches, P->npatch, da, P->st, k, S->d_stage_off, S->sbuf, S->stage_total);
+    PCUDA(cudaGetLastError());
+    for (const PlaneRun& r : S->runs) {
+      // patches of the run that still have plane k (nz may differ)
+      int p0 = r.p0;
+      while (p0 < r.p1) {
+        if (k >= P->hp[p0].nz) { ++p0; continue; }
+        int p1 = p0 + 1;
+        while (p1 < r.p1 && k < P->hp[p1].nz) ++p1;
+        const long long o = S->stage_off[p0];
+        const long long nplanes = p1 - p0;
+        int rc = dst_gemm(S->handle, r.Q, r.nx, S->sbuf + o, S->shat + o, nplanes * r.ny);
+        if (rc) return rc;
+        plane_modal_thomas_kernel<<<(unsigned)((nplanes * r.nx + 127) / 128), 128, 0, s>>>(r.d_fac, S->shat + o,
+                                                                                           nplanes);
+        PCUDA(cudaGetLastError());
+        rc = dst_gemm(S->handle, r.Q, r.nx, S->shat + o, S->sbuf + o, nplanes * r.ny);
+        if (rc) return rc;
+        p0 = p1;
+      }
+    }
+    plane_stage_relax_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega, k,
+                                                                            S->d_stage_off, S->sbuf, S->stage_total);
+    PCUDA(cudaGetLastError());
+  }
+  return PSM_OK;
+}
