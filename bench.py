@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""Benchmark: G unknown-updates/s per fp64 smoothing sweep and % of HBM roofline.
+
+Workload (BASELINE.json configs[4], the one the metric's 1/2/4/8-GPU figure is
+quoted on): a 1024^3 uniform grid, line block Jacobi (block_dims (1024,1,1),
+omega 0.8), z-slab decomposed over N GPUs (one process per GPU, launched by
+torchrun for N > 1); strong scaling, the global grid is fixed.  A step is one
+smoother step as the reference runs it (smoother.py:138-153): the line-Jacobi
+sweep with its fused residual-norm partials, the buffer swap, the physical
+ghost refresh and, for N > 1, the NCCL halo exchange overlapped with the
+interior sweep.
+
+Keys beyond the base contract:
+  roofline      dominant kernel (line Jacobi sweep) achieved GB/s from 24
+                algorithmic bytes per update (read u, read f, write v) over its
+                CUDA-event duration inside the timed region, vs the measured
+                copy bandwidth in MEASURED_PEAKS.json
+  cpu_baseline  the oracle's C restatement (OpenMP, all host cores) on a
+                bounded slab of the same workload ("port": the reference is pure
+                Python with no native code to build)
+  e2e           the same metric through the public API with host buffers:
+                per call H2D of u and f from pinned memory, smooth(...) with
+                --e2e-sweeps sweeps including the history, D2H of u + history
+`--impl reference` runs only the CPU port on rank 0 (see cpu_baseline).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Gunknown-updates/s per smoothing sweep (fp64) and % of HBM roofline, 1/2/4/8 GPU"
+UNIT = "Gupdates/s"
+BYTES_PER_UPDATE = 24  # read u 8, read f 8, write v 8
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--shape", type=int, nargs=3, default=(1024, 1024, 1024))
+    ap.add_argument("--e2e-sweeps", type=int, default=10)
+    ap.add_argument("--e2e-calls", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU port (oracle/psm_oracle.c) -- the reference arm and cpu_baseline
+# ---------------------------------------------------------------------------
+def _oracle_lib():
+    path = os.path.join(ROOT, "oracle", "build", "liboracle.so")
+    if not os.path.exists(path):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
+    lib = ctypes.CDLL(path)
+    lib.oracle_line_jacobi.restype = ctypes.c_double
+    lib.oracle_line_jacobi.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3 + [
+        ctypes.c_double, ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int]
+    lib.oracle_fill_ghosts.argtypes = [ctypes.c_void_p] + [ctypes.c_int] * 4
+    lib.oracle_max_threads.restype = ctypes.c_int
+    return lib
+
+
+class CpuPort:
+    """One bounded slab (nx x ny x 8 planes) of the workload on the host."""
+
+    def __init__(self, nx, ny, nz=8):
+        import numpy as np
+
+        self.lib = _oracle_lib()
+        self.threads = os.cpu_count() or 1
+        self.shape = (nx, ny, nz)
+        rng = np.random.default_rng(42)
+        pad = (nz + 2, ny + 2, nx + 2)
+        self.u = np.zeros(pad)
+        self.v = np.zeros(pad)
+        self.u[1:-1, 1:-1, 1:-1] = rng.random((nz, ny, nx))
+        self.f = rng.standard_normal((nz, ny, nx))
+        self.faces = (ctypes.c_double * 6)(*([-1.0] * 6))
+        self.lib.oracle_fill_ghosts(self.u.ctypes.data, nx, ny, nz, self.threads)
+
+    @property
+    def cells(self):
+        return self.shape[0] * self.shape[1] * self.shape[2]
+
+    def step(self):
+        nx, ny, nz = self.shape
+        self.lib.oracle_line_jacobi(self.u.ctypes.data, self.f.ctypes.data, self.v.ctypes.data, nx, ny, nz, 6.0,
+                                    self.faces, 0.8, 1, self.threads)
+        self.u, self.v = self.v, self.u
+        self.lib.oracle_fill_ghosts(self.u.ctypes.data, nx, ny, nz, self.threads)
+
+    def rate(self, seconds=None, steps=None, warmup=1):
+        for _ in range(warmup):
+            self.step()
+        n, t0 = 0, time.perf_counter()
+        while True:
+            self.step()
+            n += 1
+            el = time.perf_counter() - t0
+            if (steps is not None and n >= steps) or (steps is None and el >= seconds):
+                break
+        return self.cells * n / el / 1e9, n, el
+
+    def describe(self, value, n, el):
+        nx, ny, nz = self.shape
+        return {
+            "value": value,
+            "unit": UNIT,
+            "cores": self.threads,
+            "kind": "port",
+            "sample": f"{n} line-Jacobi sweeps (+ghost fill, fused norm) of a {nx}x{ny}x{nz} slab of the "
+                      f"workload ({el:.1f} s), oracle/psm_oracle.c with {self.threads} OpenMP threads",
+        }
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy, of measured)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM, "B200_PROFILING.md fallback 6.65 TB/s (of fallback)"
+
+
+def _traffic(workload_key):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(workload_key)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    nx, ny, _ = args.shape
+    port = CpuPort(nx, ny, 8)
+    value, n, el = port.rate(steps=args.steps, warmup=args.warmup)
+    cb = port.describe(value, n, el)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": el / n * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: u0 ~ U[0,1) (default_rng(42)), f ~ N(0,1), host memory",
+        "config": {"workload": f"C5 bounded sample: {nx}x{ny}x8 slab of the {args.shape[0]}^3 line-Jacobi grid",
+                   "block_dims": [nx, 1, 1], "omega": 0.8},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1208_1975_b200 as ps
+    from paper_1208_1975_b200 import _lib
+    from paper_1208_1975_b200.dist import SlabDomain, dist_smooth, jacobi_step_overlapped
+    from paper_1208_1975_b200.smoother import _Plan
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    nx, ny, nz = args.shape
+    dom = SlabDomain((nx, ny, nz), rank, world, device=dev, group=None) if world > 1 else None
+    if dom is None:
+        # single GPU: the same class without a process group
+        dom = SlabDomain((nx, ny, nz), 0, 1, device=dev)
+    p = dom.patch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    p.interior.copy_(torch.rand(p.interior.shape, generator=gen, device=dev, dtype=torch.float64))
+    p.f.copy_(torch.randn(p.f.shape, generator=gen, device=dev, dtype=torch.float64))
+    cfg = ps.SmootherConfig(scheme="block_jacobi", block_dims=(nx, 1, 1), omega=0.8, steps=1,
+                            strategy=ps.ExecutionStrategy.device(devices=world))
+    cache = ps.InverseCache()
+    plan = _Plan(dom.level, cfg, cache)
+    dp = plan.dev
+    dp.reserve(2)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # initial ghosts (physical + halo)
+    dp.refresh(_lib.GHOST_ALL)
+    if world > 1:
+        dom.finish_exchange(dom.start_exchange(p._active))
+        dom.unpack(dp)
+
+    sweep_events = []
+
+    def step(s, record):
+        # the sweep launches are bracketed by events on the launching stream
+        if record:
+            a = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        jacobi_step_overlapped(dom, dp, cfg.omega, s % 2) if world > 1 else _single_step(s)
+        if record:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record(stream)
+            sweep_events.append((a, b))
+
+    act_buf = (ctypes.c_ubyte * 1)()
+    sweep_only = []
+
+    def _single_step(s):
+        act_buf[0] = p._active
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(lib.psm_jacobi_sweep(dp.handle, act_buf, cfg.omega, s % 2, ctypes.c_void_p(stream.cuda_stream)),
+                   "jacobi_sweep")
+        e1.record(stream)
+        sweep_only.append((e0, e1))
+        p.swap_buffers()
+        dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+
+    for s in range(args.warmup):
+        step(s, False)
+    sweep_only.clear()
+    torch.cuda.synchronize(dev)
+    barrier()
+    launches0 = lib.psm_plan_launches(dp.handle)
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize(dev)
+        start.record(stream)
+        for s in range(args.steps):
+            step(s, True)
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+    launches = lib.psm_plan_launches(dp.handle) - launches0
+    ms = start.elapsed_time(stop)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    cells = nx * ny * nz
+    value = cells * args.steps / (ms_total / 1e3) / 1e9
+    # dominant kernel: the sweep (single launch per step on 1 GPU; on N GPUs
+    # the step's three range launches are bracketed together with the halo)
+    if sweep_only:
+        sweep_ms = sum(a.elapsed_time(b) for a, b in sweep_only) / len(sweep_only)
+    else:
+        sweep_ms = sum(a.elapsed_time(b) for a, b in sweep_events) / len(sweep_events)
+    local_cells = p.dims.interior_cells
+    achieved = BYTES_PER_UPDATE * local_cells / (sweep_ms / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    roofline = {
+        "bound": "hbm",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": achieved / peak,
+        "traffic": _traffic(f"line_jacobi_{nx}x{ny}x{p.dims.nz}"),
+        "kernel": "psm::line_tile_kernel<1> (line Jacobi sweep, fused residual norm + x ghosts)",
+        "bytes_per_launch": BYTES_PER_UPDATE * local_cells,
+        "avg_launch_ms": sweep_ms,
+        "peak_source": peak_src,
+        "frac_of_nominal_8000": achieved / 8000.0,
+    }
+    clocks = clk.summary()
+
+    # ---- e2e through the public API with host buffers ---------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(args, dom, cfg, cache, dev, world, rank)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        port = CpuPort(nx, ny, 8)
+        v, n, el = port.rate(seconds=args.cpu_seconds)
+        cpu = port.describe(v, n, el)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic: u0 ~ U[0,1), f ~ N(0,1) from a per-rank seeded device generator",
+            "config": {
+                "workload": f"C5: {nx}x{ny}x{nz} uniform grid, line block Jacobi, z-slabs over {world} GPU(s)",
+                "global_shape": [nx, ny, nz],
+                "block_dims": [nx, 1, 1],
+                "omega": 0.8,
+                "parallelism": f"z-slab x{world}",
+                "step": "sweep (+fused norm, x ghosts) + swap + physical ghosts (+ NCCL halo, overlapped)",
+                "l2": "no flush: inputs 25.8 GB per sweep >> 126 MB L2",
+            },
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def _e2e(args, dom, cfg, cache, dev, world, rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1208_1975_b200 as ps
+    from paper_1208_1975_b200.dist import dist_smooth
+
+    p = dom.patch
+    sweeps = args.e2e_sweeps
+    ecfg = ps.SmootherConfig(scheme="block_jacobi", block_dims=cfg.block_dims, omega=0.8, steps=sweeps,
+                             strategy=cfg.strategy)
+    host_u = torch.empty(p._bufs[0].shape, dtype=torch.float64, pin_memory=True)
+    host_f = torch.empty(p._f.shape, dtype=torch.float64, pin_memory=True)
+    host_u.copy_(p._bufs[p._active])
+    host_f.copy_(p._f)
+    out_u = torch.empty_like(host_u, pin_memory=True)
+
+    def call():
+        p._active = 0
+        p._bufs[0].copy_(host_u, non_blocking=True)
+        p._f.copy_(host_f, non_blocking=True)
+        hist = dist_smooth(dom, ecfg, cache) if world > 1 else ps.smooth(dom.level, ecfg, cache)[1]
+        out_u.copy_(p._bufs[p._active], non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return hist
+
+    call()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_calls):
+        hist = call()
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el = float(t.item())
+    nx, ny, nz = dom.global_shape
+    value = nx * ny * nz * sweeps * args.e2e_calls / el / 1e9
+    h2d = (host_u.numel() + host_f.numel()) * 8 * world
+    d2h = (out_u.numel() * 8 + (sweeps + 1) * 8) * world
+    assert all(math.isfinite(h) for h in hist)
+    return {
+        "value": value,
+        "unit": UNIT,
+        "h2d_bytes_per_step": h2d,
+        "d2h_bytes_per_step": d2h,
+        "step": f"one smooth() call: H2D u,f (pinned) + {sweeps} sweeps with history + D2H u + history",
+        "calls": args.e2e_calls,
+        "seconds": el,
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -109,6 +109,22 @@ int psm_residual(psm_plan* plan, const unsigned char* active, int slot, void* st
  * of the current iterate) goes to slot `slot` (slot < 0: not recorded). */
 int psm_jacobi_sweep(psm_plan* plan, const unsigned char* active, double omega, int slot, void* stream);
 
+/* The same sweep restricted to planes [k0, k1) of one patch (line plans):
+ * lets a multi-GPU step sweep its boundary planes first and overlap the halo
+ * exchange with the interior planes.  Same arithmetic and slot layout. */
+int psm_jacobi_sweep_planes(psm_plan* plan, const unsigned char* active, double omega, int slot, int patch, int k0,
+                            int k1, void* stream);
+
+/* exchange_interface_ghosts for a copy whose source patch lives on another
+ * GPU (grid.py:523-547): copies the interior nx*ny cells of a received
+ * contiguous padded plane (px*py doubles, device) into z-ghost plane `side`
+ * (0: k = -1, 1: k = nz) of the active buffer of `patch`. */
+int psm_halo_unpack(psm_plan* plan, const unsigned char* active, int patch, int side, const double* plane_dev,
+                    void* stream);
+
+/* Number of kernels this plan has launched so far (benchmark evidence). */
+long long psm_plan_launches(const psm_plan* plan);
+
 /* One block Gauss-Seidel sweep in place (smoother.py:156-169, ghosts lagged).
  * mode PSM_GS_WAVEFRONT reproduces the serial lexicographic order exactly;
  * PSM_GS_CHAOTIC runs lines without ordering guarantees. */

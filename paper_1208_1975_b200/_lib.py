@@ -47,6 +47,9 @@ EXPORTS = (
     "psm_history_sumsq",
     "psm_history_planes",
     "psm_tree_sum",
+    "psm_jacobi_sweep_planes",
+    "psm_halo_unpack",
+    "psm_plan_launches",
 )
 
 
@@ -118,6 +121,9 @@ def load():
             "psm_history_sumsq": (i, [vp, i, ctypes.POINTER(d), vp]),
             "psm_history_planes": (i, [vp, i, vp, vp]),
             "psm_tree_sum": (i, [vp, ll, vp, vp]),
+            "psm_jacobi_sweep_planes": (i, [vp, ub, d, i, i, i, i, vp]),
+            "psm_halo_unpack": (i, [vp, ub, i, i, vp, vp]),
+            "psm_plan_launches": (ll, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -14,13 +14,18 @@
 
 namespace psm {
 cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
-                              const StencilDev& st, double omega, double* partials, double* rbuf, long long ntiles,
-                              int threads, size_t smem, cudaStream_t stream);
+                              const StencilDev& st, double omega, double* partials, double* rbuf, long long tile_base,
+                              long long ntiles, int threads, size_t smem, cudaStream_t stream);
 cudaError_t launch_line_generic(int solve, const PatchDev* patches, int npatch, const unsigned char* active,
-                                const StencilDev& st, double omega, double* partials, long long ntiles,
-                                cudaStream_t stream);
+                                const StencilDev& st, double omega, double* partials, long long tile_base,
+                                long long ntiles, cudaStream_t stream);
 cudaError_t launch_line_apply(const LineFac* L, const double* r, double* x, long long count, cudaStream_t stream);
 cudaError_t line_tile_kernel_setup(size_t smem);
+bool line_nx_specialised(int nx);
+int line_nx_occupancy(int nx);
+cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
+                           const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
+                           cudaStream_t stream);
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
                                    const long long* gprefix, long long total, int skip_x, cudaStream_t stream);
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
@@ -28,6 +33,7 @@ cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char
 cudaError_t launch_plane_sums(const PatchDev* patches, int npatch, const double* partials, double* plane_sums,
                               int nplanes, cudaStream_t stream);
 cudaError_t launch_tree_sum(const double* in, long long n, double* out, cudaStream_t stream);
+cudaError_t launch_halo_unpack(double* dst_plane, const double* src_plane, int px, int py, cudaStream_t stream);
 cudaError_t launch_line_gs(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, int* flags, long long nunits,
                            const int* unit_patch, const int* unit_plane, int threads, size_t smem, int grid,
@@ -277,8 +283,9 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     h.nx = d.nx;
     h.ny = d.ny;
     h.nz = d.nz;
-    h.R = P->tiled ? largest_divisor_le(d.ny, std::max(1, kMaxTileCells / d.nx)) : 1;
-    h.tiles = (d.ny / h.R) * d.nz;
+    h.R = P->tiled ? std::max(1, kMaxTileCells / d.nx) : 1;
+    h.tpp = (d.ny + h.R - 1) / h.R;
+    h.tiles = h.tpp * d.nz;
     h.tile0 = tile0;
     h.plane0 = plane0;
     h.lf = (kind == PSM_BLOCK_LINE) ? P->fac[p]->d_line : nullptr;
@@ -431,11 +438,15 @@ int psm_refresh_ghosts(psm_plan* P, const unsigned char* active, int what, void*
   int rc = get_active(P, active, &da);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (what & PSM_GHOST_PHYSICAL)
+  if (what & PSM_GHOST_PHYSICAL) {
     CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->d_gprefix, P->ghost_total,
                                     (what & PSM_GHOST_SKIP_X) ? 1 : 0, s));
-  if (what & PSM_GHOST_INTERFACE)
+    P->launches += P->ghost_total > 0;
+  }
+  if (what & PSM_GHOST_INTERFACE) {
     CUDA_TRY(launch_interface_copies(P->d_patches, da, P->d_copies, P->ncopy, P->copy_total, s));
+    P->launches += (P->ncopy > 0 && P->copy_total > 0);
+  }
   return PSM_OK;
 }
 
@@ -448,13 +459,54 @@ int psm_residual(psm_plan* P, const unsigned char* active, int slot, void* strea
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (P->tiled) {
-    CUDA_TRY(launch_line_tiles(0, P->d_patches, P->npatch, da, P->st, 0.0, part, nullptr, P->ntiles, P->threads, 0, s));
+    CUDA_TRY(launch_line_tiles(0, P->d_patches, P->npatch, da, P->st, 0.0, part, nullptr, 0, P->ntiles, P->threads, 0, s));
   } else {
-    CUDA_TRY(launch_line_generic(0, P->d_patches, P->npatch, da, P->st, 0.0, part, P->ntiles, s));
+    CUDA_TRY(launch_line_generic(0, P->d_patches, P->npatch, da, P->st, 0.0, part, 0, P->ntiles, s));
   }
+  P->launches += 1;
   return PSM_OK;
 }
 
+
+// Launch the line-Jacobi sweep over global tiles [t0, t1): consecutive
+// patches that share a specialised nx run the persistent nx kernel, the rest
+// the generic tile kernel; each group is one launch.
+static int sweep_tiles(psm_plan* P, const unsigned char* da, double omega, double* part, long long t0, long long t1,
+                       cudaStream_t s) {
+  if (!P->tiled) {
+    CUDA_TRY(launch_line_generic(1, P->d_patches, P->npatch, da, P->st, omega, part, t0, t1 - t0, s));
+    P->launches += 1;
+    return PSM_OK;
+  }
+  const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
+                    P->st.zm == -1.0 && P->st.zp == -1.0;
+  int p = 0;
+  while (p < P->npatch && P->hp[p].tile0 + P->hp[p].tiles <= t0) ++p;
+  while (p < P->npatch && P->hp[p].tile0 < t1) {
+    const int nx = P->hp[p].nx;
+    const bool spec = line_nx_specialised(nx);
+    int q = p + 1;
+    while (q < P->npatch && P->hp[q].tile0 < t1 && P->hp[q].nx == nx) ++q;
+    const long long a = std::max(t0, P->hp[p].tile0);
+    const long long b = std::min(t1, P->hp[q - 1].tile0 + P->hp[q - 1].tiles);
+    if (spec) {
+      int& grid = P->nx_grid[nx];
+      if (grid == 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = std::max(1, line_nx_occupancy(nx)) * sms;
+      }
+      CUDA_TRY(launch_line_nx(nx, unit ? 1 : 0, P->d_patches, P->npatch, da, P->st, omega, part, a, b, grid, s));
+    } else {
+      CUDA_TRY(launch_line_tiles(1, P->d_patches, P->npatch, da, P->st, omega, part, nullptr, a, b - a, P->threads,
+                                 P->smem, s));
+    }
+    P->launches += 1;
+    p = q;
+  }
+  return PSM_OK;
+}
 
 int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int slot, void* stream) {
   if (!P) return fail(PSM_EINVAL, "null plan");
@@ -465,18 +517,45 @@ int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int
   double* part = slot_ptr(P, slot, &rc);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (P->kind == PSM_BLOCK_LINE) {
-    if (P->tiled) {
-      CUDA_TRY(launch_line_tiles(1, P->d_patches, P->npatch, da, P->st, omega, part, nullptr, P->ntiles, P->threads,
-                                 P->smem, s));
-    } else {
-      CUDA_TRY(launch_line_generic(1, P->d_patches, P->npatch, da, P->st, omega, part, P->ntiles, s));
-    }
-    return PSM_OK;
-  }
+  if (P->kind == PSM_BLOCK_LINE) return sweep_tiles(P, da, omega, part, 0, P->ntiles, s);
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_jacobi(P, da, omega, part, s);
   return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
 }
+
+int psm_jacobi_sweep_planes(psm_plan* P, const unsigned char* active, double omega, int slot, int patch, int k0,
+                            int k1, void* stream) {
+  if (!P) return fail(PSM_EINVAL, "null plan");
+  if (P->kind != PSM_BLOCK_LINE) return fail(PSM_EUNSUPPORTED, "plane-range sweeps are implemented for line plans");
+  if (!(omega > 0.0 && omega <= 1.0)) return fail(PSM_EINVAL, "omega must lie in (0, 1], got %g", omega);
+  if (patch < 0 || patch >= P->npatch) return fail(PSM_EINVAL, "bad patch %d", patch);
+  const PatchDev& h = P->hp[patch];
+  if (k0 < 0 || k1 > h.nz || k0 > k1) return fail(PSM_EINVAL, "bad plane range [%d,%d) for nz=%d", k0, k1, h.nz);
+  unsigned char* da;
+  int rc = get_active(P, active, &da);
+  if (rc) return rc;
+  double* part = slot_ptr(P, slot, &rc);
+  if (rc) return rc;
+  const long long tpp = h.tpp;  // tiles per plane
+  const long long t0 = h.tile0 + k0 * tpp, nt = (long long)(k1 - k0) * tpp;
+  if (nt == 0) return PSM_OK;
+  return sweep_tiles(P, da, omega, part, t0, t0 + nt, (cudaStream_t)stream);
+}
+
+int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int side, const double* plane_dev,
+                    void* stream) {
+  if (!P || !active || !plane_dev) return fail(PSM_EINVAL, "bad arguments");
+  if (patch < 0 || patch >= P->npatch || (side != 0 && side != 1)) return fail(PSM_EINVAL, "bad patch/side");
+  const PatchDev& h = P->hp[patch];
+  const int a = active[patch];
+  if (a != 0 && a != 1) return fail(PSM_EINVAL, "active flags must be 0 or 1");
+  const long long px = h.nx + 2, py = h.ny + 2, pz = h.nz + 2;
+  double* dst = h.buf[a] + (side ? (pz - 1) : 0) * px * py;
+  CUDA_TRY(launch_halo_unpack(dst, plane_dev, (int)px, (int)py, (cudaStream_t)stream));
+  P->launches += 1;
+  return PSM_OK;
+}
+
+long long psm_plan_launches(const psm_plan* P) { return P ? P->launches : -1; }
 
 
 // Work units (patch, plane) in dependency order and the progress flags of
@@ -534,6 +613,7 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
     }
     for (int d = 0; d < maxd; ++d)
       CUDA_TRY(launch_line_gs_generic(P->d_patches, P->npatch, da, P->st, omega, d, nj, s));
+    P->launches += maxd;
     return PSM_OK;
   }
   rc = psm_line_gs_prepare(P);
@@ -541,6 +621,7 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
   CUDA_TRY(cudaMemsetAsync(P->d_flags, 0, (P->nplanes + 1) * sizeof(int), s));
   CUDA_TRY(launch_line_gs(mode, P->d_patches, P->npatch, da, P->st, omega, P->d_flags + 1, P->nunits,
                           P->d_unit_patch, P->d_unit_plane, P->gs_threads, P->gs_smem, P->gs_grid, s));
+  P->launches += 1;
   return PSM_OK;
 }
 
@@ -553,6 +634,7 @@ int psm_history_sumsq(psm_plan* P, int nslots, double* out_host, void* stream) {
     double* ps = P->d_plane_sums + (size_t)k * std::max(1, P->nplanes);
     CUDA_TRY(launch_plane_sums(P->d_patches, P->npatch, P->d_partials + k * tstride, ps, P->nplanes, s));
     CUDA_TRY(launch_tree_sum(ps, P->nplanes, P->d_sums + k, s));
+    P->launches += 2;
   }
   if (nslots > 0) {
     CUDA_TRY(cudaMemcpyAsync(out_host, P->d_sums, nslots * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -103,7 +103,7 @@ __global__ void plane_sums_kernel(const PatchDev* __restrict__ patches, int npat
   }
   const PatchDev& P = patches[lo];
   const int k = gp - P.plane0;
-  const int per = P.ny / P.R;
+  const int per = P.tpp;
   const double* src = partials + P.tile0 + (long long)k * per;
   double s = 0.0;
   for (int t = 0; t < per; ++t) s += src[t];
@@ -128,6 +128,28 @@ __global__ void __launch_bounds__(1024) tree_sum_kernel(const double* __restrict
     __syncthreads();
   }
   if (t == 0) out[0] = buf[0];
+}
+
+// Interface ghosts from a remote rank: the interior (nx x ny) of a received
+// contiguous padded plane goes into one z-ghost plane (grid.py:541-546 for a
+// copy whose source lives on another GPU; edges stay physical as in the
+// reference, whose InterfaceCopy extents never include edge cells).
+__global__ void halo_unpack_kernel(double* __restrict__ dst_plane, const double* __restrict__ src_plane, int px,
+                                   int py) {
+  const long long n = (long long)(px - 2) * (py - 2);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (px - 2)) + 1, j = (int)(t / (px - 2)) + 1;
+    const long long o = (long long)j * px + i;
+    dst_plane[o] = src_plane[o];
+  }
+}
+
+cudaError_t launch_halo_unpack(double* dst_plane, const double* src_plane, int px, int py, cudaStream_t stream) {
+  const long long n = (long long)(px - 2) * (py - 2);
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  halo_unpack_kernel<<<(unsigned)blocks, 256, 0, stream>>>(dst_plane, src_plane, px, py);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,

@@ -49,8 +49,9 @@ struct PatchDev {
   double* buf[2];
   const double* f;
   int nx, ny, nz;
-  int R;          // rows (x-lines) per tile, divides ny
-  int tiles;      // ny*nz/R
+  int R;          // rows (x-lines) per tile (the last tile of a plane may be short)
+  int tpp;        // tiles per plane = ceil(ny / R)
+  int tiles;      // tpp * nz
   long long tile0;  // first global tile
   int plane0;     // first global plane (prefix of nz)
   long long cell0;  // first interior cell (prefix of nx*ny*nz), for plane workspaces
@@ -69,6 +70,14 @@ struct StencilDev {
 };
 
 __host__ __device__ inline int row_stride(int nx) { return nx + (nx + kSeg - 1) / kSeg; }
+
+// tile -> (plane k, first row j0, rows in this tile); tiles never straddle planes
+__device__ __forceinline__ void tile_coords(const PatchDev& P, long long tile, int& k, int& j0, int& rows) {
+  const int ti = (int)(tile - P.tile0);
+  k = ti / P.tpp;
+  j0 = (ti - k * P.tpp) * P.R;
+  rows = min(P.R, P.ny - j0);
+}
 
 __device__ __forceinline__ int find_patch(const PatchDev* __restrict__ p, int n, long long tile) {
   int lo = 0, hi = n - 1;
@@ -149,7 +158,8 @@ struct psm_plan {
   long long nunits = 0;
   int gs_threads = 0, gs_grid = 0;
   size_t gs_smem = 0;
-  int sweep_count = 0;
+  long long launches = 0;  // kernels this plan launched (bench evidence)
+  std::map<int, int> nx_grid;  // persistent grid per specialised nx
   // plane path
   PlaneState* plane = nullptr;
 };

@@ -27,18 +27,18 @@ template <int MODE>  // 0: residual partials only, 1: Jacobi sweep, 2: residual 
 __global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __restrict__ patches, int npatch,
                                                         const unsigned char* __restrict__ active, StencilDev st,
                                                         double omega, double* __restrict__ partials,
-                                                        double* __restrict__ rbuf) {
+                                                        double* __restrict__ rbuf, long long tile_base) {
   extern __shared__ double sm[];
   __shared__ double wsum[32];
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
-  const long long tile = blockIdx.x;
+  const long long tile = tile_base + blockIdx.x;
   const int pi = find_patch(patches, npatch, tile);
   const PatchDev& P = patches[pi];
-  const int nx = P.nx, ny = P.ny, R = P.R;
+  const int nx = P.nx, ny = P.ny;
   const long long cell0 = P.cell0;
   const LineFac* __restrict__ L = P.lf;
-  const int row0 = (int)(tile - P.tile0) * R;
-  const int k = row0 / ny, j0 = row0 - k * ny;
+  int k, j0, R;
+  tile_coords(P, tile, k, j0, R);
   const long long px = nx + 2, pxy = px * (ny + 2);
   const int act = active[pi];
   const double* __restrict__ u = P.buf[act];
@@ -176,15 +176,15 @@ __global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __res
 // with the relaxed value.  Tiles have R = 1 (one line per partial).
 __global__ void line_generic_jacobi_kernel(const PatchDev* __restrict__ patches, int npatch,
                                            const unsigned char* __restrict__ active, StencilDev st,
-                                           double omega, double* __restrict__ partials, long long ntiles,
-                                           int solve) {
-  const long long tile = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (tile >= ntiles) return;
+                                           double omega, double* __restrict__ partials, long long tile_base,
+                                           long long ntiles, int solve) {
+  const long long tile = tile_base + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (tile >= tile_base + ntiles) return;
   const int pi = find_patch(patches, npatch, tile);
   const PatchDev& P = patches[pi];
   const int nx = P.nx, ny = P.ny;
-  const int row = (int)(tile - P.tile0);
-  const int k = row / ny, j = row - k * ny;
+  int k, j, rows_;
+  tile_coords(P, tile, k, j, rows_);
   const long long px = nx + 2, pxy = px * (ny + 2);
   const int act = active[pi];
   const double* u = P.buf[act];
@@ -233,31 +233,264 @@ __global__ void line_apply_kernel(const LineFac* __restrict__ L, const double* _
   for (int i = nx - 2; i >= 0; --i) xb[i] = fma(-L->cpN[i], xb[i + 1], xb[i]);
 }
 
+
+// ---------------------------------------------------------------------------
+// Specialised line-Jacobi sweep for power-of-two nx in [64, 1024].
+//
+// Persistent CTAs (256 threads) walk tiles of R = 2048/NX x-lines of one
+// plane in plane-major order, so the planes k-1, k, k+1 that concurrent
+// tiles touch stay in L2 and u streams from HBM about once.  Per tile:
+//   A  8 cells per thread, coalesced LDG.64 of u (centre, y+-1, z+-1) and f,
+//      x+-1 by warp shuffle; r (reference operation order) -> shared memory,
+//      r^2 -> tile partial.
+//   B  one lane per 32-cell segment (R*NX/32 = 64 lanes): Thomas on the
+//      segment with the dependency chain shortened to one DFMA per cell
+//      (y_i = r_i*invm_i - (lo*invm_i)*y_{i-1}), segment end values swapped
+//      between neighbouring lanes by shuffle (a row's segments share a warp),
+//      interface 2x2 solves -> per-segment coefficients cl, cr.
+//   C  8 cells per thread: x = y - cl*g[i] - cr*h[i], v = u + omega*x,
+//      store v and the physical x-face ghosts of v.
+// Shared buffers are double-buffered across tiles: two barriers per tile.
+// ---------------------------------------------------------------------------
+template <int NX, int UNIT>
+__global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                                                const unsigned char* __restrict__ active,
+                                                                StencilDev st, double omega,
+                                                                double* __restrict__ partials, long long tile_begin,
+                                                                long long tile_end) {
+  constexpr int T = 256, R = kMaxTileCells / NX, NSEG = NX / kSeg, CELLS = R * NX, E = CELLS / T;
+  constexpr int RS = NX + NSEG, PX = NX + 2, NSL = R * NSEG;
+  static_assert(E == 8 && NSEG <= 32 && NSL <= T, "tile shape");
+  __shared__ double rs[2][R * RS];
+  __shared__ double cl[2][NSL], cr[2][NSL];
+  __shared__ double wsum[2][T / 32];
+  __shared__ double tab_invm[kSeg], tab_loinv[kSeg], tab_cp[kSeg], tab_g[kSeg], tab_h[kSeg];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const LineFac* lf_loaded = nullptr;
+  double lo = 0, up = 0, up_h31 = 0, lo_g0 = 0, d_full = 0;
+  int buf = 0;
+  for (long long tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x, buf ^= 1) {
+    const int pi = find_patch(patches, npatch, tile);
+    const PatchDev& P = patches[pi];
+    const LineFac* L = P.lf;
+    if (L != lf_loaded) {  // uniform across the CTA; tables for this nx
+      __syncthreads();
+      if (tid < kSeg) {
+        const double im = L->invm[tid];
+        tab_invm[tid] = im;
+        tab_loinv[tid] = L->lo * im;
+        tab_cp[tid] = L->cp[tid];
+        tab_g[tid] = L->g[tid];
+        tab_h[tid] = L->h[tid];
+      }
+      lo = L->lo;
+      up = L->up;
+      up_h31 = L->up_h31;
+      lo_g0 = L->lo_g0;
+      d_full = L->d_full;
+      lf_loaded = L;
+      __syncthreads();
+    }
+    const int ny = P.ny;
+    int k, j0, rows;
+    tile_coords(P, tile, k, j0, rows);
+    const long long pxy = (long long)PX * (ny + 2);
+    const int act = active[pi];
+    const double* __restrict__ u = P.buf[act];
+    double* __restrict__ v = P.buf[act ^ 1];
+    const long long ubase = (long long)(k + 1) * pxy + (long long)(j0 + 1) * PX + 1;
+    const double* __restrict__ fb = P.f + ((long long)k * ny + j0) * NX;
+    double* __restrict__ rb = rs[buf];
+
+    // ---- A ----------------------------------------------------------------
+    double ssq = 0.0;
+    double ucen[E];
+#pragma unroll
+    for (int h = 0; h < E; h += 4) {
+      double c[4], ym[4], yp[4], zm[4], zp[4], fv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = (h + q) * T + tid;
+        const int row = e / NX, x = e % NX;
+        const long long iu = ubase + (long long)row * PX + x;
+        if (row < rows) {
+          c[q] = __ldg(u + iu);
+          ym[q] = __ldg(u + iu - PX);
+          yp[q] = __ldg(u + iu + PX);
+          zm[q] = __ldg(u + iu - pxy);
+          zp[q] = __ldg(u + iu + pxy);
+          fv[q] = __ldg(fb + e);
+        } else {
+          c[q] = ym[q] = yp[q] = zm[q] = zp[q] = fv[q] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = (h + q) * T + tid;
+        const int row = e / NX, x = e % NX;
+        double xl = __shfl_up_sync(0xffffffffu, c[q], 1);
+        double xr = __shfl_down_sync(0xffffffffu, c[q], 1);
+        ucen[h + q] = c[q];
+        if (row < rows) {
+          const long long iu = ubase + (long long)row * PX + x;
+          if (lane == 0) xl = __ldg(u + iu - 1);
+          if (lane == 31) xr = __ldg(u + iu + 1);
+          double res;
+          if (UNIT) {
+            double acc = __dmul_rn(st.c, c[q]);
+            acc = __dsub_rn(acc, xl);
+            acc = __dsub_rn(acc, xr);
+            acc = __dsub_rn(acc, ym[q]);
+            acc = __dsub_rn(acc, yp[q]);
+            acc = __dsub_rn(acc, zm[q]);
+            acc = __dsub_rn(acc, zp[q]);
+            res = __dsub_rn(fv[q], acc);
+          } else {
+            res = residual7(st, fv[q], c[q], xl, xr, ym[q], yp[q], zm[q], zp[q]);
+          }
+          ssq = fma(res, res, ssq);
+          rb[row * RS + x + (x >> 5)] = res;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+    if (lane == 0) wsum[buf][warp] = ssq;
+    __syncthreads();  // (1) r complete
+    if (tid == 0 && partials) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < T / 32; ++w) t += wsum[buf][w];
+      partials[tile] = t;
+    }
+
+    // ---- B: segment solves + interfaces (lanes 0..NSL-1) ---------------------
+    if (tid < NSL) {
+      const int r = tid / NSEG, s = tid % NSEG;
+      double* seg = rb + r * RS + s * (kSeg + 1);
+      double yv[kSeg];
+#pragma unroll
+      for (int i = 0; i < kSeg; ++i) yv[i] = seg[i] * tab_invm[i];
+      double prev = yv[0];
+#pragma unroll
+      for (int i = 1; i < kSeg; ++i) {
+        prev = fma(-tab_loinv[i], prev, yv[i]);
+        yv[i] = prev;
+      }
+      const double ylast = prev;
+#pragma unroll
+      for (int i = kSeg - 2; i >= 0; --i) yv[i] = fma(-tab_cp[i], yv[i + 1], yv[i]);
+#pragma unroll
+      for (int i = 0; i < kSeg; ++i) seg[i] = yv[i];
+      const double yfirst = yv[0];
+      // neighbours' end values: lanes of one row are contiguous in a warp
+      const double yl_left = __shfl_up_sync(0xffffffffu >> (32 - (NSL < 32 ? NSL : 32)), ylast, 1);
+      const double yf_right = __shfl_down_sync(0xffffffffu >> (32 - (NSL < 32 ? NSL : 32)), yfirst, 1);
+      double cl_v = 0.0, cr_v = 0.0;
+      if (s > 0) cl_v = lo * ((yl_left - up_h31 * yfirst) * d_full);
+      if (s < NSEG - 1) {
+        const double xl2 = (ylast - up_h31 * yf_right) * d_full;
+        cr_v = up * (yf_right - lo_g0 * xl2);
+      }
+      cl[buf][tid] = cl_v;
+      cr[buf][tid] = cr_v;
+    }
+    __syncthreads();  // (2) y, cl, cr complete
+
+    // ---- C ----------------------------------------------------------------
+#pragma unroll
+    for (int h = 0; h < E; ++h) {
+      const int e = h * T + tid;
+      const int row = e / NX, x = e % NX;
+      if (row < rows) {
+        const int sl = row * NSEG + (x >> 5);
+        const double y = rb[row * RS + x + (x >> 5)];
+        const double xs = fma(-cr[buf][sl], tab_h[lane], fma(-cl[buf][sl], tab_g[lane], y));
+        const double nv = relax(ucen[h], omega, xs);
+        const long long iu = ubase + (long long)row * PX + x;
+        v[iu] = nv;
+        if (x == 0) v[iu - 1] = -nv;
+        if (x == NX - 1) v[iu + 1] = -nv;
+      }
+    }
+  }
+}
+
+template <int NX>
+static cudaError_t launch_nx(int unit, const PatchDev* patches, int npatch, const unsigned char* active,
+                             const StencilDev& st, double omega, double* partials, long long t0, long long t1,
+                             int grid, cudaStream_t stream) {
+  if (unit)
+    line_jacobi_nx_kernel<NX, 1><<<grid, 256, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1);
+  else
+    line_jacobi_nx_kernel<NX, 0><<<grid, 256, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1);
+  return cudaGetLastError();
+}
+
+// nx values with a specialised kernel
+bool line_nx_specialised(int nx) {
+  return nx == 64 || nx == 128 || nx == 256 || nx == 512 || nx == 1024;
+}
+
+template <int NX>
+static int occ_nx() {
+  int a = 0, b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, line_jacobi_nx_kernel<NX, 0>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, line_jacobi_nx_kernel<NX, 1>, 256, 0);
+  return a < b ? a : b;
+}
+
+int line_nx_occupancy(int nx) {
+  switch (nx) {
+    case 64: return occ_nx<64>();
+    case 128: return occ_nx<128>();
+    case 256: return occ_nx<256>();
+    case 512: return occ_nx<512>();
+    default: return occ_nx<1024>();
+  }
+}
+
+cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
+                           const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
+                           cudaStream_t stream) {
+  if (t1 <= t0) return cudaSuccess;
+  const long long n = t1 - t0;
+  if (grid > n) grid = (int)n;
+  switch (nx) {
+    case 64: return launch_nx<64>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+    case 128: return launch_nx<128>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+    case 256: return launch_nx<256>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+    case 512: return launch_nx<512>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+    case 1024: return launch_nx<1024>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // ---- host-side launchers ---------------------------------------------------
 cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
-                              const StencilDev& st, double omega, double* partials, double* rbuf, long long ntiles,
-                              int threads, size_t smem, cudaStream_t stream) {
-  if (ntiles == 0) return cudaSuccess;
+                              const StencilDev& st, double omega, double* partials, double* rbuf, long long tile_base,
+                              long long ntiles, int threads, size_t smem, cudaStream_t stream) {
+  if (ntiles <= 0) return cudaSuccess;
   if (mode == 0) {
     line_tile_kernel<0><<<(unsigned)ntiles, threads, 0, stream>>>(patches, npatch, active, st, omega, partials,
-                                                                  nullptr);
+                                                                  nullptr, tile_base);
   } else if (mode == 1) {
     line_tile_kernel<1><<<(unsigned)ntiles, threads, smem, stream>>>(patches, npatch, active, st, omega, partials,
-                                                                     nullptr);
+                                                                     nullptr, tile_base);
   } else {
     line_tile_kernel<2><<<(unsigned)ntiles, threads, 0, stream>>>(patches, npatch, active, st, omega, partials,
-                                                                  rbuf);
+                                                                  rbuf, tile_base);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_line_generic(int solve, const PatchDev* patches, int npatch, const unsigned char* active,
-                                const StencilDev& st, double omega, double* partials, long long ntiles,
-                                cudaStream_t stream) {
-  if (ntiles == 0) return cudaSuccess;
+                                const StencilDev& st, double omega, double* partials, long long tile_base,
+                                long long ntiles, cudaStream_t stream) {
+  if (ntiles <= 0) return cudaSuccess;
   const int tpb = 128;
   line_generic_jacobi_kernel<<<(unsigned)((ntiles + tpb - 1) / tpb), tpb, 0, stream>>>(
-      patches, npatch, active, st, omega, partials, ntiles, solve);
+      patches, npatch, active, st, omega, partials, tile_base, ntiles, solve);
   return cudaGetLastError();
 }
 

@@ -26,8 +26,8 @@
 
 namespace psm {
 cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
-                              const StencilDev& st, double omega, double* partials, double* rbuf, long long ntiles,
-                              int threads, size_t smem, cudaStream_t stream);
+                              const StencilDev& st, double omega, double* partials, double* rbuf, long long tile_base,
+                              long long ntiles, int threads, size_t smem, cudaStream_t stream);
 
 // r = f - A u of every cell of plane `k` of every patch with nz > k (GS
 // stage) into the compact stage buffer, rows of the same patch contiguous.
@@ -313,8 +313,9 @@ int psm_plane_plan_free(psm_plan* P) {
 // modal Thomas -> DST back -> relax into v.
 int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double* partials, cudaStream_t s) {
   PlaneState* S = P->plane;
-  PCUDA(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, S->rbuf, P->ntiles, P->threads, 0,
+  PCUDA(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, S->rbuf, 0, P->ntiles, P->threads, 0,
                           s));
+  P->launches += 2 + (long long)S->runs.size();  // residual, modal Thomas per run, relax
   cublasSetStream(S->handle, s);
   for (const PlaneRun& r : S->runs) {
     const long long c0 = P->hp[r.p0].cell0;
@@ -343,6 +344,7 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
   int maxnz = 0;
   for (auto& h : P->hp) maxnz = std::max(maxnz, h.nz);
   for (int k = 0; k < maxnz; ++k) {
+    P->launches += 2;
     plane_stage_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(
         P->d_patches, P->npatch, da, P->st, k, S->d_stage_off, S->sbuf, S->stage_total);
     PCUDA(cudaGetLastError());
@@ -359,6 +361,7 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
         if (rc) return rc;
         plane_modal_thomas_kernel<<<(unsigned)((nplanes * r.nx + 127) / 128), 128, 0, s>>>(r.d_fac, S->shat + o,
                                                                                            nplanes);
+        P->launches += 1;
         PCUDA(cudaGetLastError());
         rc = dst_gemm(S->handle, r.Q, r.nx, S->shat + o, S->sbuf + o, nplanes * r.ny);
         if (rc) return rc;

@@ -1,0 +1,224 @@
+"""Multi-GPU z-slab decomposition: one process per GPU over torch.distributed.
+
+A uniform nx x ny x nz grid is cut into contiguous z-slabs, one patch per rank
+with origin (0, 0, k0).  In reference terms this is a multi-patch ``Level``
+whose patches abut along z (``grid.py:429-465``); the only cross-rank
+``InterfaceCopy`` entries are the two z-faces of each slab.  The reference's
+semantics make the split exact for Jacobi (reference
+``test_smoother.py:164-196``): ghosts carry previous-step values, so the
+sliced run is bit-identical to the single-patch run, history included,
+because per-plane residual partial sums are all-gathered and reduced by the
+same fixed tree as on one GPU.  GS on slabs is GS on the split level
+(inter-slab coupling lagged to step end, as in the reference).
+
+Per Jacobi step on each rank (line blocks), with the halo overlapped:
+
+  sweep boundary planes (k = 0, nz-1) --event--> comm stream: NCCL send of the
+  new boundary planes to the z-neighbours, receive theirs into staging
+  | sweep interior planes | swap | physical ghosts | wait comm | unpack the
+  received planes' interiors into the z-ghost planes (psm_halo_unpack).
+
+The exchange helpers are device-agnostic (they move tensors with
+``torch.distributed``); tests drive them with world_size 2 over gloo on CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .grid import Level, Patch, PatchDims, _int3
+
+__all__ = ["slab_range", "SlabDomain", "exchange_planes", "gather_plane_sums"]
+
+
+def slab_range(nz, world, rank):
+    """[k0, k1) of rank's slab: contiguous, sizes differ by at most one."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    if nz < world:
+        raise ValueError(f"cannot cut {nz} planes into {world} slabs")
+    base, extra = divmod(nz, world)
+    k0 = rank * base + min(rank, extra)
+    return k0, k0 + base + (rank < extra)
+
+
+def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank, group=None):
+    """Send ``send_lo`` to ``lo_rank`` and ``send_hi`` to ``hi_rank``; receive
+    into ``recv_lo`` from ``lo_rank`` and ``recv_hi`` from ``hi_rank`` (None
+    ranks are skipped).  Returns the list of outstanding requests."""
+    ops = []
+    if lo_rank is not None:
+        ops.append(dist.P2POp(dist.isend, send_lo, lo_rank, group))
+        ops.append(dist.P2POp(dist.irecv, recv_lo, lo_rank, group))
+    if hi_rank is not None:
+        ops.append(dist.P2POp(dist.isend, send_hi, hi_rank, group))
+        ops.append(dist.P2POp(dist.irecv, recv_hi, hi_rank, group))
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+def gather_plane_sums(local, group=None):
+    """All-gather equal-length per-plane vectors (slots, nz_local) in rank
+    order -> (slots, world * nz_local)."""
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local.contiguous(), group=group)
+    return torch.cat(parts, dim=-1)
+
+
+class SlabDomain:
+    """This rank's slab of a global grid plus its z-neighbours."""
+
+    def __init__(self, global_shape, rank=None, world=None, device=None, group=None):
+        self.global_shape = _int3(global_shape, "global_shape")
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        self.group = group
+        nx, ny, nz = self.global_shape
+        self.k0, self.k1 = slab_range(nz, self.world, self.rank)
+        self.patch = Patch(PatchDims(nx, ny, self.k1 - self.k0), origin=(0, 0, self.k0), device=device)
+        # a one-patch level: every face of the slab is physical locally; the
+        # cross-rank z faces are overwritten by the exchange (physical first,
+        # interface second, as grid.py:507-517)
+        self.level = Level([self.patch])
+        self.lo_rank = self.rank - 1 if self.rank > 0 else None
+        self.hi_rank = self.rank + 1 if self.rank < self.world - 1 else None
+        px, py = nx + 2, ny + 2
+        dev = self.patch.device
+        self.stage_lo = torch.zeros((py, px), dtype=torch.float64, device=dev)
+        self.stage_hi = torch.zeros((py, px), dtype=torch.float64, device=dev)
+        self._comm_stream = torch.cuda.Stream(dev) if dev.type == "cuda" else None
+
+    @property
+    def nz_local(self):
+        return self.k1 - self.k0
+
+    def boundary_planes(self, buf_index):
+        """Contiguous padded planes k = 0 and k = nz_local-1 of buffer ``buf_index``."""
+        b = self.patch._bufs[buf_index]
+        return b[1], b[self.nz_local]
+
+    def start_exchange(self, buf_index):
+        """Send the boundary planes of buffer ``buf_index`` to the neighbours
+        and receive theirs into the staging planes (on the comm stream when
+        on CUDA).  Returns the requests; call ``finish_exchange`` after."""
+        lo, hi = self.boundary_planes(buf_index)
+        if self._comm_stream is None:
+            return exchange_planes(lo, hi, self.stage_lo, self.stage_hi, self.lo_rank, self.hi_rank, self.group)
+        main = torch.cuda.current_stream(self.patch.device)
+        self._comm_stream.wait_stream(main)
+        with torch.cuda.stream(self._comm_stream):
+            reqs = exchange_planes(lo, hi, self.stage_lo, self.stage_hi, self.lo_rank, self.hi_rank, self.group)
+            for r in reqs:
+                r.wait()
+        return reqs
+
+    def finish_exchange(self, reqs):
+        if self._comm_stream is None:
+            for r in reqs:
+                r.wait()
+            return
+        torch.cuda.current_stream(self.patch.device).wait_stream(self._comm_stream)
+
+    def unpack(self, plan):
+        """Received planes -> z-ghost planes of the active buffer (device)."""
+        lib = _lib.load()
+        act = (ctypes.c_ubyte * 1)(self.patch._active)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(self.patch.device).cuda_stream)
+        if self.lo_rank is not None:
+            _lib.check(lib.psm_halo_unpack(plan.handle, act, 0, 0, ctypes.c_void_p(self.stage_lo.data_ptr()),
+                                           stream), "halo_unpack")
+        if self.hi_rank is not None:
+            _lib.check(lib.psm_halo_unpack(plan.handle, act, 0, 1, ctypes.c_void_p(self.stage_hi.data_ptr()),
+                                           stream), "halo_unpack")
+
+
+def dist_smooth(domain, config, cache, record_history=True):
+    """``smooth`` on a z-slab decomposed grid: every rank calls it with its
+    own ``SlabDomain``; returns the (global) history on every rank."""
+    from .smoother import _Plan, _gs_mode
+
+    level = domain.level
+    plan = _Plan(level, config, cache)
+    dp = plan.dev
+    lib = _lib.load()
+    steps = config.steps
+    nzl = domain.nz_local
+    with torch.cuda.device(plan.device):
+        dp.reserve(steps + 1)
+        dp.refresh(_lib.GHOST_ALL)
+        reqs = domain.start_exchange(domain.patch._active)
+        domain.finish_exchange(reqs)
+        domain.unpack(dp)
+        if config.scheme == "block_jacobi" and plan.kind == "line":
+            for s in range(steps):
+                jacobi_step_overlapped(domain, dp, config.omega, s)
+            dp.residual(steps)
+        else:
+            mode = _gs_mode(config)
+            if config.scheme != "block_jacobi":
+                dp.residual(0)
+            for s in range(steps):
+                if config.scheme == "block_jacobi":
+                    dp.jacobi(config.omega, s)
+                    domain.patch.swap_buffers()
+                    dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+                else:
+                    dp.gs(config.omega, mode)
+                    dp.refresh(_lib.GHOST_ALL)
+                reqs = domain.start_exchange(domain.patch._active)
+                domain.finish_exchange(reqs)
+                domain.unpack(dp)
+                if config.scheme != "block_jacobi":
+                    dp.residual(s + 1)
+            if config.scheme == "block_jacobi":
+                dp.residual(steps)
+        if not record_history:
+            return None
+        planes = torch.empty((steps + 1, nzl), dtype=torch.float64, device=plan.device)
+        for s in range(steps + 1):
+            dp.plane_sums(s, planes[s])
+        full = gather_plane_sums(planes, domain.group)
+        out = torch.empty(steps + 1, dtype=torch.float64, device=plan.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(plan.device).cuda_stream)
+        for s in range(steps + 1):
+            row = full[s].contiguous()
+            _lib.check(lib.psm_tree_sum(ctypes.c_void_p(row.data_ptr()), row.numel(),
+                                        ctypes.c_void_p(out[s:].data_ptr()), stream), "tree_sum")
+        return [math.sqrt(v) for v in out.cpu().tolist()]
+
+
+def jacobi_step_overlapped(domain, dp, omega, slot):
+    """One line-Jacobi step of a slab with the halo exchange overlapped with
+    the interior sweep (see the module docstring)."""
+    lib = _lib.load()
+    p = domain.patch
+    nzl = domain.nz_local
+    act = (ctypes.c_ubyte * 1)(p._active)
+    stream = ctypes.c_void_p(torch.cuda.current_stream(p.device).cuda_stream)
+
+    def sweep(k0, k1):
+        if k1 > k0:
+            _lib.check(lib.psm_jacobi_sweep_planes(dp.handle, act, float(omega), slot, 0, k0, k1, stream),
+                       "jacobi_sweep_planes")
+
+    if domain.world == 1:
+        sweep(0, nzl)
+        p.swap_buffers()
+        dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+        return
+    sweep(0, 1)
+    sweep(nzl - 1, nzl) if nzl > 1 else None
+    new = 1 - p._active  # the buffer the sweep writes
+    reqs = domain.start_exchange(new)
+    sweep(1, nzl - 1)
+    p.swap_buffers()
+    dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+    domain.finish_exchange(reqs)
+    domain.unpack(dp)

@@ -1,0 +1,123 @@
+"""The multi-GPU z-slab path's host logic on CPU: world_size 2 over gloo.
+
+Each rank owns a z-slab (``dist.SlabDomain``), runs the oracle's line-Jacobi
+sweep on its slab (standing in for the CUDA kernel, which needs a GPU), and
+uses the product's exchange code (``start_exchange`` / ``finish_exchange``,
+``gather_plane_sums``) for the halo planes and the history.  The assembled
+result must equal the single-domain oracle bit for bit (Jacobi slab splits
+are exact), history included."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import restate as R
+
+SHAPE = (24, 10, 12)
+STEPS = 4
+OMEGA = 0.8
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _fview(t):
+    return t.numpy().transpose(2, 1, 0)  # F-ordered (px, py, pz) view
+
+
+def _inputs():
+    rng = np.random.default_rng(17)
+    return rng.standard_normal(SHAPE), rng.standard_normal(SHAPE)
+
+
+def _rank_main(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1208_1975_b200.dist import SlabDomain, gather_plane_sums
+
+        dom = SlabDomain(SHAPE, rank, world, device="cpu")
+        u0, f = _inputs()
+        p = dom.patch
+        p.interior[...] = torch.from_numpy(np.ascontiguousarray(u0[:, :, dom.k0:dom.k1]))
+        p.f[...] = torch.from_numpy(np.ascontiguousarray(f[:, :, dom.k0:dom.k1]))
+        fl = _fview(p._f)
+
+        def refresh():
+            u = _fview(p._bufs[p._active])
+            R.fill_physical_ghosts(u)
+            reqs = dom.start_exchange(p._active)
+            dom.finish_exchange(reqs)
+            if dom.lo_rank is not None:
+                u[1:-1, 1:-1, 0] = _fview(dom.stage_lo[None])[1:-1, 1:-1, 0]
+            if dom.hi_rank is not None:
+                u[1:-1, 1:-1, -1] = _fview(dom.stage_hi[None])[1:-1, 1:-1, 0]
+
+        def plane_sums():
+            u = _fview(p._bufs[p._active])
+            r = R.residual(u, fl)
+            return np.array([np.sum(np.square(r[:, :, k])) for k in range(dom.nz_local)])
+
+        refresh()
+        sums = []
+        for _ in range(STEPS):
+            u = _fview(p._bufs[p._active])
+            v = _fview(p._bufs[1 - p._active])
+            sums.append(plane_sums())
+            r = R.residual(u, fl)
+            v[1:-1, 1:-1, 1:-1] = u[1:-1, 1:-1, 1:-1] + OMEGA * R.line_solve(r)
+            p.swap_buffers()
+            refresh()
+        sums.append(plane_sums())
+        full = gather_plane_sums(torch.from_numpy(np.stack(sums)))
+        hist = [math.sqrt(float(np.sum(row))) for row in full.numpy()]
+        np.save(os.path.join(out_dir, f"slab{rank}.npy"), p.interior.numpy())
+        np.save(os.path.join(out_dir, f"hist{rank}.npy"), np.array(hist))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_slab_jacobi_equals_single_domain(tmp_path):
+    world = 2
+    mp.spawn(_rank_main, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    u0, f = _inputs()
+    o = R.OPatch(SHAPE)
+    o.u[1:-1, 1:-1, 1:-1] = u0
+    o.f[:] = f
+    lv = R.OLevel([o])
+    lv.refresh_ghosts()
+    want_hist = []
+    for _ in range(STEPS):
+        r = R.residual(o.u, o.f)
+        want_hist.append(math.sqrt(sum(np.sum(np.square(r[:, :, k])) for k in range(SHAPE[2]))))
+        R.jacobi_step(lv, (SHAPE[0], 1, 1), OMEGA)
+    r = R.residual(o.u, o.f)
+    want_hist.append(math.sqrt(sum(np.sum(np.square(r[:, :, k])) for k in range(SHAPE[2]))))
+    got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)], axis=2)
+    np.testing.assert_array_equal(got, o.interior)
+    for r in range(world):
+        h = np.load(tmp_path / f"hist{r}.npy")
+        np.testing.assert_allclose(h, want_hist, rtol=1e-14, atol=0)
+    np.testing.assert_array_equal(np.load(tmp_path / "hist0.npy"), np.load(tmp_path / "hist1.npy"))
+
+
+@pytest.mark.parametrize("nz,world", [(12, 2), (13, 4), (1024, 8), (9, 3)])
+def test_slab_ranges_tile_the_grid(nz, world):
+    from paper_1208_1975_b200.dist import slab_range
+
+    spans = [slab_range(nz, world, r) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == nz
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 1

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     text = open(os.path.join(ROOT, "include", "psmooth.h")).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(psm_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|long long|const char\*)\s+(psm_\w+)\(", text, re.M)))
 
 
 def test_header_declares_what_binding_uses():
