@@ -22,6 +22,10 @@ cudaError_t launch_line_generic(int solve, const PatchDev* patches, int npatch, 
 cudaError_t launch_line_apply(const LineFac* L, const double* r, double* x, long long count, cudaStream_t stream);
 cudaError_t line_tile_kernel_setup(size_t smem);
 bool line_nx_specialised(int nx);
+int zmarch_rows(int nx);
+cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
+                               const StencilDev& st, double omega, double* partials, const void* units, int nunits,
+                               int grid, cudaStream_t stream);
 int line_nx_occupancy(int nx);
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
@@ -157,6 +161,22 @@ static int build_line(const psm_stencil* st, int nx, psm_factors* F) {
   L.lo_gT0 = (double)(lo * gT[0]);
   L.d_full = (double)(1.0L / (1.0L - up * lo * h[kSeg - 1] * g[0]));
   L.d_tail = (double)(1.0L / (1.0L - up * lo * h[kSeg - 1] * gT[0]));
+  {
+    long double e16[16], g16[16], h16[16];
+    for (int i = 0; i < 16; ++i) e16[i] = 0;
+    e16[0] = 1;
+    thomas_ld(16, c, lo, up, e16, g16);
+    e16[0] = 0;
+    e16[15] = 1;
+    thomas_ld(16, c, lo, up, e16, h16);
+    for (int i = 0; i < 16; ++i) {
+      L.g16[i] = (double)g16[i];
+      L.h16[i] = (double)h16[i];
+    }
+    L.up_h16 = (double)(up * h16[15]);
+    L.lo_g16 = (double)(lo * g16[0]);
+    L.d16 = (double)(1.0L / (1.0L - up * lo * h16[15] * g16[0]));
+  }
   // couplings dropped by the 2x2 interface systems
   const long double dropped = fabsl(lo * g[kSeg - 1]) + fabsl(up * h[0]);
   L.partitioned = (L.nseg == 1) || (dropped < 1e-18L);
@@ -370,6 +390,7 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_flags);
   cudaFree(P->d_unit_patch);
   cudaFree(P->d_unit_plane);
+  for (auto& kv : P->unit_cache) cudaFree(kv.second.first);
   for (auto& kv : P->active_cache) cudaFree(kv.second);
   if (P->kind == PSM_BLOCK_PLANE) psm_plane_plan_free(P);
   delete P;
@@ -468,41 +489,80 @@ int psm_residual(psm_plan* P, const unsigned char* active, int slot, void* strea
 }
 
 
-// Launch the line-Jacobi sweep over global tiles [t0, t1): consecutive
-// patches that share a specialised nx run the persistent nx kernel, the rest
-// the generic tile kernel; each group is one launch.
-static int sweep_tiles(psm_plan* P, const unsigned char* da, double omega, double* part, long long t0, long long t1,
-                       cudaStream_t s) {
-  if (!P->tiled) {
-    CUDA_TRY(launch_line_generic(1, P->d_patches, P->npatch, da, P->st, omega, part, t0, t1 - t0, s));
-    P->launches += 1;
+// z-marching work units (patch, j0, k0, k1) for planes [ka, kb) of patches
+// [p0, p1) -- patch-major, then plane chunk, then column, so concurrently
+// running CTAs march neighbouring columns through the same planes.  Cached.
+static int zmarch_units(psm_plan* P, int p0, int p1, int ka, int kb, void** d_units, int* nunits) {
+  const std::string key = std::to_string(p0) + ":" + std::to_string(p1) + ":" + std::to_string(ka) + ":" +
+                          std::to_string(kb);
+  auto it = P->unit_cache.find(key);
+  if (it != P->unit_cache.end()) {
+    *d_units = it->second.first;
+    *nunits = it->second.second;
     return PSM_OK;
   }
+  long long cols = 0;
+  for (int p = p0; p < p1; ++p) cols += P->hp[p].tpp;
+  const long long planes = std::max(1, (kb < 0 ? P->hp[p0].nz : kb) - ka);
+  const long long target = 8LL * 148;
+  int kc = (int)std::min<long long>(128, std::max<long long>(4, cols * planes / target));
+  std::vector<int> u;
+  for (int p = p0; p < p1; ++p) {
+    const PatchDev& h = P->hp[p];
+    const int a = ka, b = (kb < 0) ? h.nz : kb;
+    for (int k0 = a; k0 < b; k0 += kc)
+      for (int c = 0; c < h.tpp; ++c) {
+        u.push_back(p);
+        u.push_back(c * h.R);
+        u.push_back(k0);
+        u.push_back(std::min(b, k0 + kc));
+      }
+  }
+  void* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, std::max<size_t>(16, u.size() * sizeof(int))));
+  CUDA_TRY(cudaMemcpy(d, u.data(), u.size() * sizeof(int), cudaMemcpyHostToDevice));
+  P->unit_cache[key] = {d, (int)(u.size() / 4)};
+  *d_units = d;
+  *nunits = (int)(u.size() / 4);
+  return PSM_OK;
+}
+
+// Line-Jacobi sweep of planes [ka, kb) (kb < 0: all planes) of patches
+// [pa, pb): consecutive patches sharing a specialised nx run the z-marching
+// TMA kernel (one launch per group), the rest the generic tile kernel.
+static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, double* part, int pa, int pb, int ka,
+                        int kb, cudaStream_t s) {
   const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
                     P->st.zm == -1.0 && P->st.zp == -1.0;
-  int p = 0;
-  while (p < P->npatch && P->hp[p].tile0 + P->hp[p].tiles <= t0) ++p;
-  while (p < P->npatch && P->hp[p].tile0 < t1) {
+  int p = pa;
+  while (p < pb) {
     const int nx = P->hp[p].nx;
-    const bool spec = line_nx_specialised(nx);
     int q = p + 1;
-    while (q < P->npatch && P->hp[q].tile0 < t1 && P->hp[q].nx == nx) ++q;
-    const long long a = std::max(t0, P->hp[p].tile0);
-    const long long b = std::min(t1, P->hp[q - 1].tile0 + P->hp[q - 1].tiles);
-    if (spec) {
-      int& grid = P->nx_grid[nx];
-      if (grid == 0) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = std::max(1, line_nx_occupancy(nx)) * sms;
-      }
-      CUDA_TRY(launch_line_nx(nx, unit ? 1 : 0, P->d_patches, P->npatch, da, P->st, omega, part, a, b, grid, s));
+    while (q < pb && P->hp[q].nx == nx) ++q;
+    if (P->tiled && line_nx_specialised(nx) && P->hp[p].R == zmarch_rows(nx)) {
+      void* units;
+      int nu;
+      int rc = zmarch_units(P, p, q, ka, kb, &units, &nu);
+      if (rc) return rc;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms, s));
+      P->launches += 1;
     } else {
-      CUDA_TRY(launch_line_tiles(1, P->d_patches, P->npatch, da, P->st, omega, part, nullptr, a, b - a, P->threads,
-                                 P->smem, s));
+      for (int r = p; r < q; ++r) {
+        const PatchDev& h = P->hp[r];
+        const int a = ka, b = (kb < 0) ? h.nz : kb;
+        const long long t0 = h.tile0 + (long long)a * h.tpp, nt = (long long)(b - a) * h.tpp;
+        if (P->tiled) {
+          CUDA_TRY(launch_line_tiles(1, P->d_patches, P->npatch, da, P->st, omega, part, nullptr, t0, nt, P->threads,
+                                     P->smem, s));
+        } else {
+          CUDA_TRY(launch_line_generic(1, P->d_patches, P->npatch, da, P->st, omega, part, t0, nt, s));
+        }
+        P->launches += 1;
+      }
     }
-    P->launches += 1;
     p = q;
   }
   return PSM_OK;
@@ -517,7 +577,7 @@ int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int
   double* part = slot_ptr(P, slot, &rc);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (P->kind == PSM_BLOCK_LINE) return sweep_tiles(P, da, omega, part, 0, P->ntiles, s);
+  if (P->kind == PSM_BLOCK_LINE) return sweep_planes(P, da, omega, part, 0, P->npatch, 0, -1, s);
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_jacobi(P, da, omega, part, s);
   return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
 }
@@ -535,10 +595,8 @@ int psm_jacobi_sweep_planes(psm_plan* P, const unsigned char* active, double ome
   if (rc) return rc;
   double* part = slot_ptr(P, slot, &rc);
   if (rc) return rc;
-  const long long tpp = h.tpp;  // tiles per plane
-  const long long t0 = h.tile0 + k0 * tpp, nt = (long long)(k1 - k0) * tpp;
-  if (nt == 0) return PSM_OK;
-  return sweep_tiles(P, da, omega, part, t0, t0 + nt, (cudaStream_t)stream);
+  if (k1 == k0) return PSM_OK;
+  return sweep_planes(P, da, omega, part, patch, patch + 1, k0, k1, (cudaStream_t)stream);
 }
 
 int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int side, const double* plane_dev,

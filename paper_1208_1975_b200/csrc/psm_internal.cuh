@@ -27,6 +27,8 @@ struct LineFac {
   double up_h31;                // up * h[31]
   double lo_g0, lo_gT0;         // lo * g[0], lo * gT[0]
   double d_full, d_tail;        // 1/(1 - up*lo*h31*g0), same with gT0
+  double g16[16], h16[16];      // spikes of a 16-cell half segment
+  double up_h16, lo_g16, d16;   // up*h16[15], lo*g16[0], 1/(1 - up*lo*h16[15]*g16[0])
   int nx, nseg, tail;
   int partitioned;              // 1: segment kernel valid; 0: generic kernel
   // generic full-length Thomas factors (device pointers into the same
@@ -160,6 +162,7 @@ struct psm_plan {
   size_t gs_smem = 0;
   long long launches = 0;  // kernels this plan launched (bench evidence)
   std::map<int, int> nx_grid;  // persistent grid per specialised nx
+  std::map<std::string, std::pair<void*, int>> unit_cache;  // z-marching units per plane range
   // plane path
   PlaneState* plane = nullptr;
 };

@@ -1,0 +1,431 @@
+// Line-block Jacobi sweep, z-marching TMA pipeline (sm_100a).
+//
+// Replaces smoother._jacobi_step + block_residual + block_update/matvec
+// (smoother.py:138-153, stencil.py:93-112, blocklinalg.py:90-105) for line
+// blocks (>=nx,1,1) and power-of-two nx in [64, 1024].
+//
+// Work unit: one column of R = 2048/nx consecutive x-lines (rows j0..j0+R-1)
+// over a chunk of planes k0..k1-1 of one patch.  Persistent CTAs (one per SM)
+// take units in (patch, chunk, column) order, so concurrently running CTAs
+// march neighbouring columns through the same planes and the y-halo rows one
+// CTA re-reads are L2 hits; u and f stream from HBM once (24 B/update).
+//
+// Warp roles (608 threads):
+//   warp 18      producer: cp.async.bulk (TMA, 1-D) of each plane's u slab
+//                (R+2 padded rows incl. both y-halo rows, contiguous in
+//                memory) into a 4-slot ring and of f's R rows into a 2-slot
+//                ring, completion via mbarrier transaction counts.
+//   warps 0-15   A/C: each thread owns 4 cells of the column and keeps a
+//                register queue u(k-1), u(k), u(k+1) for them, so per plane it
+//                reads only the new plane's centre, u(j+-1) and f from shared
+//                memory; x+-1 come by warp shuffle.  A(k): residual in the
+//                reference operation order -> padded r buffer, r^2 partial.
+//                C(k-1): x = y - cl*g - cr*h, v = u + omega*x, store v and
+//                the physical x-face ghosts of v.
+//   warps 16-17  solver: one lane per 32-cell segment (64 segments per tile):
+//                Thomas with constant factors, segment ends exchanged by
+//                shuffle, exact 2x2 interface solves -> cl, cr; also the
+//                tile's r^2 partial.  B(k) overlaps A(k+1) of the A/C warps
+//                (double-buffered r / y buffers, named barriers).
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "psm_internal.cuh"
+
+namespace psm {
+
+struct ZUnit {
+  int patch, j0, k0, k1;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "MBW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBW_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int NX>
+struct ZCfg {
+  static constexpr int R = kMaxTileCells / NX;  // rows per column
+  static constexpr int PX = NX + 2;
+  static constexpr int NSEG = NX / kSeg;
+  static constexpr int NSL = R * NSEG;  // 64 segment lanes
+  static constexpr int RS = NX + NSEG;  // padded r row
+  static constexpr int NU = 4, NF = 2;  // ring slots
+  static constexpr int US = (R + 2) * PX;  // doubles per u slot
+  static constexpr int FS = R * NX;
+  static constexpr int RB = R * RS;
+  static constexpr int AC_WARPS = 16, SOLVER_WARPS = 2, THREADS = (AC_WARPS + SOLVER_WARPS + 1) * 32;
+  static constexpr int ACT = AC_WARPS * 32;
+  static constexpr int E = kMaxTileCells / ACT;  // cells per A/C thread (4)
+  static constexpr size_t SMEM_DOUBLES = (size_t)NU * US + NF * FS + 2 * RB + 4 * NSL + 2 * AC_WARPS + 7 * kSeg;
+  static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * 8 + (2 * NU + 2 * NF) * 8 + 16;
+};
+
+constexpr int kBarR = 1, kBarY = 3;
+
+// cell q of A/C thread tid (0..ACT-1) in a tile of 2048/NX rows: cells
+// e = q*ACT + tid, row = e / NX, x = e % NX, folded at compile time
+template <int NX, int ACT>
+__device__ __forceinline__ int cell_row(int q, int tid) {
+  if constexpr (NX >= ACT) return (q * ACT) / NX;
+  else return q * (ACT / NX) + tid / NX;
+}
+template <int NX, int ACT>
+__device__ __forceinline__ int cell_x(int q, int tid) {
+  if constexpr (NX >= ACT) return (q * ACT) % NX + tid;
+  else return tid % NX;
+}  // named barriers 1,2 (r ready) and 3,4 (y ready)
+
+template <int NX, int UNIT>
+__global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
+    line_jacobi_zmarch_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
+                              StencilDev st, double omega, double* __restrict__ partials,
+                              const ZUnit* __restrict__ units, int nunits) {
+  using C = ZCfg<NX>;
+  constexpr int R = C::R, PX = C::PX, NSEG = C::NSEG, NSL = C::NSL, RS = C::RS, E = C::E, ACT = C::ACT;
+  extern __shared__ __align__(128) double zsm[];
+  double* uring = zsm;
+  double* fring = uring + C::NU * C::US;
+  double* rbuf = fring + C::NF * C::FS;
+  double* clb = rbuf + 2 * C::RB;
+  double* crb = clb + 2 * NSL;
+  double* wsum = crb + 2 * NSL;
+  double* tab = wsum + 2 * C::AC_WARPS;  // invm, loinv, cp, g, h, g16|h16
+  uint64_t* bars = (uint64_t*)(tab + 7 * kSeg);
+  uint64_t* full_u = bars;
+  uint64_t* empty_u = full_u + C::NU;
+  uint64_t* full_f = empty_u + C::NU;
+  uint64_t* empty_f = full_f + C::NF;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < C::NU; ++s) {
+      mbar_init(&full_u[s], 1);
+      mbar_init(&empty_u[s], C::AC_WARPS);
+    }
+    for (int s = 0; s < C::NF; ++s) {
+      mbar_init(&full_f[s], 1);
+      mbar_init(&empty_f[s], C::AC_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // factor tables: every patch of one launch shares nx and the stencil, so
+  // the first unit's LineFac serves all (psm_api.cu groups launches by nx)
+  if (tid < kSeg && nunits > 0) {
+    const LineFac* L = patches[units[0].patch].lf;
+    const double im = L->invm[tid];
+    tab[tid] = im;
+    tab[kSeg + tid] = L->lo * im;
+    tab[2 * kSeg + tid] = L->cp[tid];
+    tab[3 * kSeg + tid] = L->g[tid];
+    tab[4 * kSeg + tid] = L->h[tid];
+    tab[5 * kSeg + tid] = L->g16[tid & 15];  // [5k..5k+15] g16, [5k+16..] h16
+    if (tid >= 16) tab[5 * kSeg + tid] = L->h16[tid - 16];
+  }
+  __syncthreads();
+
+  // ======================= producer warp =====================================
+  if (warp == C::AC_WARPS + C::SOLVER_WARPS) {
+    if (lane != 0) return;
+    uint32_t nu = 0, nf = 0;
+    for (int w = blockIdx.x; w < nunits; w += gridDim.x) {
+      const ZUnit U = units[w];
+      const PatchDev& P = patches[U.patch];
+      const int rows = min(R, P.ny - U.j0);
+      const long long pxy = (long long)PX * (P.ny + 2);
+      const double* u = P.buf[active[U.patch]];
+      const uint32_t ubytes = (uint32_t)((rows + 2) * PX * 8);
+      const uint32_t fbytes = (uint32_t)(rows * NX * 8);
+      for (int kk = U.k0 - 1; kk <= U.k1; ++kk) {
+        // u slab of plane kk: rows j0-1 .. j0+rows, contiguous
+        const int s = nu % C::NU;
+        mbar_wait(&empty_u[s], ((nu / C::NU) & 1) ^ 1);
+        mbar_expect_tx(&full_u[s], ubytes);
+        tma_load_1d(uring + s * C::US, u + (long long)(kk + 1) * pxy + (long long)U.j0 * PX, ubytes, &full_u[s]);
+        ++nu;
+        // f slab of plane kk-1 once its u(k+1) partner is queued
+        const int kf = kk - 1;
+        if (kf >= U.k0 && kf < U.k1) {
+          const int t = nf % C::NF;
+          mbar_wait(&empty_f[t], ((nf / C::NF) & 1) ^ 1);
+          mbar_expect_tx(&full_f[t], fbytes);
+          tma_load_1d(fring + t * C::FS, P.f + ((long long)kf * P.ny + U.j0) * NX, fbytes, &full_f[t]);
+          ++nf;
+        }
+      }
+    }
+    return;
+  }
+
+  // ======================= solver warps ======================================
+  if (warp >= C::AC_WARPS) {
+    const int sl = tid - C::AC_WARPS * 32;  // 0..NSL-1
+    const int r = sl / NSEG, s = sl % NSEG;
+    const LineFac* L = patches[units[0].patch].lf;
+    const double lo = L->lo, up = L->up, up_h31 = L->up_h31, lo_g0 = L->lo_g0, d_full = L->d_full;
+    const double up_h16 = L->up_h16, lo_g16 = L->lo_g16, d16 = L->d16;
+    int b = 0;
+    for (int w = blockIdx.x; w < nunits; w += gridDim.x) {
+      const ZUnit U = units[w];
+      const PatchDev& P = patches[U.patch];
+      for (int k = U.k0; k < U.k1; ++k, b ^= 1) {
+        named_sync(kBarR + b, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
+        if (sl == 0 && partials) {
+          double t = 0.0;
+#pragma unroll
+          for (int q = 0; q < C::AC_WARPS; ++q) t += wsum[b * C::AC_WARPS + q];
+          partials[P.tile0 + (long long)k * P.tpp + U.j0 / R] = t;
+        }
+        double* seg = rbuf + b * C::RB + r * RS + s * (kSeg + 1);
+        // local solve of the 32-cell segment as two independent 16-cell
+        // Thomas chains (same prefix factors) joined by an exact 2x2 system
+        double ya[16], yb[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          ya[i] = seg[i] * tab[i];
+          yb[i] = seg[16 + i] * tab[i];
+        }
+#pragma unroll
+        for (int i = 1; i < 16; ++i) {
+          ya[i] = fma(-tab[kSeg + i], ya[i - 1], ya[i]);
+          yb[i] = fma(-tab[kSeg + i], yb[i - 1], yb[i]);
+        }
+#pragma unroll
+        for (int i = 14; i >= 0; --i) {
+          ya[i] = fma(-tab[2 * kSeg + i], ya[i + 1], ya[i]);
+          yb[i] = fma(-tab[2 * kSeg + i], yb[i + 1], yb[i]);
+        }
+        const double xa15 = (ya[15] - up_h16 * yb[0]) * d16;
+        const double xb0 = yb[0] - lo_g16 * xa15;
+        const double ca = up * xb0, cb = lo * xa15;
+        double yv[kSeg];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          yv[i] = fma(-ca, tab[5 * kSeg + 16 + i], ya[i]);
+          yv[16 + i] = fma(-cb, tab[5 * kSeg + i], yb[i]);
+        }
+        const double ylast = yv[kSeg - 1];
+#pragma unroll
+        for (int i = 0; i < kSeg; ++i) seg[i] = yv[i];
+        const double yfirst = yv[0];
+        const double yl_left = __shfl_up_sync(0xffffffffu, ylast, 1);
+        const double yf_right = __shfl_down_sync(0xffffffffu, yfirst, 1);
+        double clv = 0.0, crv = 0.0;
+        if (s > 0) clv = lo * ((yl_left - up_h31 * yfirst) * d_full);
+        if (s < NSEG - 1) crv = up * (yf_right - lo_g0 * ((ylast - up_h31 * yf_right) * d_full));
+        clb[b * NSL + sl] = clv;
+        crb[b * NSL + sl] = crv;
+        named_arrive(kBarY + b, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
+      }
+    }
+    return;
+  }
+
+  // ======================= A/C warps =========================================
+  const double* tg = tab + 3 * kSeg;
+  const double* th = tab + 4 * kSeg;
+  const double tgl = tg[lane], thl = th[lane];
+  uint32_t nu = 0, nf = 0;
+  int b = 0;
+  for (int w = blockIdx.x; w < nunits; w += gridDim.x) {
+    const ZUnit U = units[w];
+    const PatchDev& P = patches[U.patch];
+    const int rows = min(R, P.ny - U.j0);
+    const long long pxy = (long long)PX * (P.ny + 2);
+    double* v = P.buf[active[U.patch] ^ 1];
+    double zm[E], c[E], zp[E], cold[E];
+    long long vbase_old = 0;
+    // slab k0-1 -> zm
+    {
+      const int s = nu % C::NU;
+      mbar_wait(&full_u[s], (nu / C::NU) & 1);
+      const double* sl = uring + s * C::US;
+#pragma unroll
+      for (int q = 0; q < E; ++q) zm[q] = sl[(cell_row<NX, ACT>(q, tid) + 1) * PX + cell_x<NX, ACT>(q, tid) + 1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_u[s]);
+      ++nu;
+    }
+    // slab k0 -> c (slot kept for the y-neighbours)
+    int s_cur = nu % C::NU;
+    mbar_wait(&full_u[s_cur], (nu / C::NU) & 1);
+    ++nu;
+    {
+      const double* sl = uring + s_cur * C::US;
+#pragma unroll
+      for (int q = 0; q < E; ++q) c[q] = sl[(cell_row<NX, ACT>(q, tid) + 1) * PX + cell_x<NX, ACT>(q, tid) + 1];
+    }
+    // C: x = y - cl*g - cr*h, v = u + omega*x (previous plane's buffers)
+    auto phaseC = [&](auto full_t) {
+      constexpr bool FULL = decltype(full_t)::value;
+      const int bo = b ^ 1;
+      named_sync(kBarY + bo, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
+      const double* yb = rbuf + bo * C::RB;
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int row = cell_row<NX, ACT>(q, tid), x = cell_x<NX, ACT>(q, tid);
+        if (FULL || row < rows) {
+          const int sg = row * NSEG + (x >> 5);
+          const double xs = fma(-crb[bo * NSL + sg], thl, fma(-clb[bo * NSL + sg], tgl, yb[row * RS + x + (x >> 5)]));
+          const double nv = relax(cold[q], omega, xs);
+          const long long iu = vbase_old + (long long)row * PX + x;
+          v[iu] = nv;
+          if constexpr (NX >= ACT) {
+            if ((q * ACT) % NX == 0 && tid == 0) v[iu - 1] = -nv;
+            if ((q * ACT) % NX == NX - ACT && tid == ACT - 1) v[iu + 1] = -nv;
+          } else {
+            if (x == 0) v[iu - 1] = -nv;
+            if (x == NX - 1) v[iu + 1] = -nv;
+          }
+        }
+      }
+    };
+    // A: residual of plane k
+    auto phaseA = [&](auto full_t, const double* cur, const double* nxt, const double* fs, double* rb) {
+      constexpr bool FULL = decltype(full_t)::value;
+      double ssq = 0.0;
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int row = cell_row<NX, ACT>(q, tid), x = cell_x<NX, ACT>(q, tid);
+        zp[q] = nxt[(row + 1) * PX + x + 1];
+        double xl = __shfl_up_sync(0xffffffffu, c[q], 1);
+        double xr = __shfl_down_sync(0xffffffffu, c[q], 1);
+        if (lane == 0) xl = cur[(row + 1) * PX + x];
+        if (lane == 31) xr = cur[(row + 1) * PX + x + 2];
+        if (FULL || row < rows) {
+          const double ym = cur[row * PX + x + 1];
+          const double yp = cur[(row + 2) * PX + x + 1];
+          const double fv = fs[row * NX + x];
+          double res;
+          if (UNIT) {
+            double acc = __dmul_rn(st.c, c[q]);
+            acc = __dsub_rn(acc, xl);
+            acc = __dsub_rn(acc, xr);
+            acc = __dsub_rn(acc, ym);
+            acc = __dsub_rn(acc, yp);
+            acc = __dsub_rn(acc, zm[q]);
+            acc = __dsub_rn(acc, zp[q]);
+            res = __dsub_rn(fv, acc);
+          } else {
+            res = residual7(st, fv, c[q], xl, xr, ym, yp, zm[q], zp[q]);
+          }
+          ssq = fma(res, res, ssq);
+          rb[row * RS + x + (x >> 5)] = res;
+        }
+      }
+      return ssq;
+    };
+    const bool full = rows == R;
+    for (int k = U.k0; k < U.k1; ++k) {
+      const int s_nxt = nu % C::NU;
+      mbar_wait(&full_u[s_nxt], (nu / C::NU) & 1);
+      ++nu;
+      const int t = nf % C::NF;
+      mbar_wait(&full_f[t], (nf / C::NF) & 1);
+      ++nf;
+      const double* cur = uring + s_cur * C::US;
+      const double* nxt = uring + s_nxt * C::US;
+      const double* fs = fring + t * C::FS;
+      double* rb = rbuf + b * C::RB;
+      double ssq = full ? phaseA(std::true_type{}, cur, nxt, fs, rb) : phaseA(std::false_type{}, cur, nxt, fs, rb);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+      if (lane == 0) wsum[b * C::AC_WARPS + warp] = ssq;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_u[s_cur]);
+        mbar_arrive(&empty_f[t]);
+      }
+      named_arrive(kBarR + b, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
+      if (k > U.k0) {
+        if (full) phaseC(std::true_type{}); else phaseC(std::false_type{});
+      }
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        cold[q] = c[q];
+        zm[q] = c[q];
+        c[q] = zp[q];
+      }
+      vbase_old = (long long)(k + 1) * pxy + (long long)(U.j0 + 1) * PX + 1;
+      s_cur = s_nxt;
+      b ^= 1;
+    }
+    // the unit's last slab (plane k1) is done; C of its last plane
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_u[s_cur]);
+    if (full) phaseC(std::true_type{}); else phaseC(std::false_type{});
+  }
+}
+
+template <int NX>
+static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned char* active, const StencilDev& st,
+                           double omega, double* partials, const ZUnit* units, int nunits, int grid,
+                           cudaStream_t stream) {
+  using C = ZCfg<NX>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM_BYTES);
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM_BYTES);
+    attr = true;
+  }
+  if (unit)
+    line_jacobi_zmarch_kernel<NX, 1><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega,
+                                                                                  partials, units, nunits);
+  else
+    line_jacobi_zmarch_kernel<NX, 0><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega,
+                                                                                  partials, units, nunits);
+  return cudaGetLastError();
+}
+
+int zmarch_rows(int nx) { return kMaxTileCells / nx; }
+
+cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
+                               const StencilDev& st, double omega, double* partials, const void* units, int nunits,
+                               int grid, cudaStream_t stream) {
+  if (nunits <= 0) return cudaSuccess;
+  if (grid > nunits) grid = nunits;
+  const ZUnit* u = (const ZUnit*)units;
+  switch (nx) {
+    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
+    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
+    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
+    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
+    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace psm
