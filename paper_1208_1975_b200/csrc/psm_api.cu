@@ -25,7 +25,7 @@ bool line_nx_specialised(int nx);
 int zmarch_rows(int nx);
 cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
                                const StencilDev& st, double omega, double* partials, const void* units, int nunits,
-                               int grid, cudaStream_t stream);
+                               int grid, const LineFac& L, cudaStream_t stream);
 int line_nx_occupancy(int nx);
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
@@ -547,7 +547,8 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms, s));
+      CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms,
+                                   P->fac[p]->h_line, s));
       P->launches += 1;
     } else {
       for (int r = p; r < q; ++r) {

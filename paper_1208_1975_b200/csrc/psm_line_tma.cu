@@ -88,11 +88,19 @@ struct ZCfg {
   static constexpr int AC_WARPS = 16, SOLVER_WARPS = 2, THREADS = (AC_WARPS + SOLVER_WARPS + 1) * 32;
   static constexpr int ACT = AC_WARPS * 32;
   static constexpr int E = kMaxTileCells / ACT;  // cells per A/C thread (4)
-  static constexpr size_t SMEM_DOUBLES = (size_t)NU * US + NF * FS + 2 * RB + 4 * NSL + 2 * AC_WARPS + 7 * kSeg;
+  static constexpr size_t SMEM_DOUBLES = (size_t)NU * US + NF * FS + 2 * RB + 2 * AC_WARPS;
   static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * 8 + (2 * NU + 2 * NF) * 8 + 16;
 };
 
 constexpr int kBarR = 1, kBarY = 3;
+
+// Factor tables passed by value: they live in the kernel-parameter constant
+// bank, so the fully unrolled solver reads them as DFMA constant operands
+// (no load instructions).
+struct ZTab {
+  double invm[kSeg], loinv[kSeg], cp[kSeg], g[kSeg], h[kSeg], g16[16], h16[16];
+  double lo, up, up_h31, lo_g0, d_full, up_h16, lo_g16, d16;
+};
 
 // cell q of A/C thread tid (0..ACT-1) in a tile of 2048/NX rows: cells
 // e = q*ACT + tid, row = e / NX, x = e % NX, folded at compile time
@@ -107,22 +115,167 @@ __device__ __forceinline__ int cell_x(int q, int tid) {
   else return tid % NX;
 }  // named barriers 1,2 (r ready) and 3,4 (y ready)
 
+// A/C warp role of the z-marching kernel.  Thread t owns NXP x-positions
+// and RPT consecutive rows of the column (E = NXP*RPT = 4 cells), so the
+// y-neighbours inside its rows come from its own registers; only the first
+// row's y-1 and the last row's y+1 are read from the slab.  Three register
+// arrays rotate through the roles u(k-1), u(k), u(k+1) (the plane loop is
+// unrolled by three, so the queue never moves data).
+template <int NX, int UNIT>
+struct ZAC {
+  using C = ZCfg<NX>;
+  static constexpr int R = C::R, PX = C::PX, RS = C::RS, E = C::E, ACT = C::ACT;
+  static constexpr bool NX_GE = NX >= ACT;
+  static constexpr int NXP = NX_GE ? NX / ACT : 1;
+  static constexpr int RPT = E / NXP;
+  static constexpr int NBAR = (C::AC_WARPS + C::SOLVER_WARPS) * 32;
+
+  int tid, lane, warp, tx, trow0, rows, j0, k0;
+  StencilDev st;
+  double omega;
+  double *uring, *fring, *rbuf, *wsum, *v;
+  uint64_t *full_u, *empty_u, *full_f, *empty_f;
+  long long pxy, vbase_old = 0;
+  uint32_t nu = 0, nf = 0;
+  int b = 0, s_cur = 0;
+  double A0[E], A1[E], A2[E];
+
+  __device__ __forceinline__ void load_c(double (&dst)[E], const double* sl) const {
+#pragma unroll
+    for (int p = 0; p < NXP; ++p)
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) dst[p * RPT + r] = sl[(trow0 + r + 1) * PX + tx + p * ACT + 1];
+  }
+
+  template <bool FULL>
+  __device__ __forceinline__ void phaseC(const double (&cold)[E]) {
+    const int bo = b ^ 1;
+    named_sync(kBarY + bo, NBAR);
+    const double* xb = rbuf + bo * C::RB;
+#pragma unroll
+    for (int p = 0; p < NXP; ++p)
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int row = trow0 + r, x = tx + p * ACT;
+        if (FULL || row < rows) {
+          const double nv = relax(cold[p * RPT + r], omega, xb[row * RS + x + (x >> 5)]);
+          const long long iu = vbase_old + (long long)row * PX + x;
+          v[iu] = nv;
+          if constexpr (NX_GE) {
+            if (p == 0 && tid == 0) v[iu - 1] = -nv;
+            if (p == NXP - 1 && tid == ACT - 1) v[iu + 1] = -nv;
+          } else {
+            if (x == 0) v[iu - 1] = -nv;
+            if (x == NX - 1) v[iu + 1] = -nv;
+          }
+        }
+      }
+  }
+
+  // plane k: A(k) then C(k-1)
+  template <bool FULL>
+  __device__ __forceinline__ void step(const double (&zm)[E], const double (&c)[E], double (&zp)[E], int k) {
+    const int s_nxt = nu % C::NU;
+    mbar_wait(&full_u[s_nxt], (nu / C::NU) & 1);
+    ++nu;
+    const int t = nf % C::NF;
+    mbar_wait(&full_f[t], (nf / C::NF) & 1);
+    ++nf;
+    const double* cur = uring + s_cur * C::US;
+    const double* fs = fring + t * C::FS;
+    double* rb = rbuf + b * C::RB;
+    load_c(zp, uring + s_nxt * C::US);
+    double ssq = 0.0;
+#pragma unroll
+    for (int p = 0; p < NXP; ++p) {
+      const int x = tx + p * ACT;
+      const double ym0 = cur[trow0 * PX + x + 1];              // y-1 of the first owned row
+      const double ypl = cur[(trow0 + RPT + 1) * PX + x + 1];  // y+1 of the last owned row
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = p * RPT + r, row = trow0 + r;
+        double xl = __shfl_up_sync(0xffffffffu, c[i], 1);
+        double xr = __shfl_down_sync(0xffffffffu, c[i], 1);
+        if (lane == 0) xl = cur[(row + 1) * PX + x];
+        if (lane == 31) xr = cur[(row + 1) * PX + x + 2];
+        if (FULL || row < rows) {
+          const double ym = r > 0 ? c[i - 1] : ym0;
+          const double yp = r < RPT - 1 ? c[i + 1] : ypl;
+          const double fv = fs[row * NX + x];
+          double res;
+          if (UNIT) {
+            double acc = __dmul_rn(st.c, c[i]);
+            acc = __dsub_rn(acc, xl);
+            acc = __dsub_rn(acc, xr);
+            acc = __dsub_rn(acc, ym);
+            acc = __dsub_rn(acc, yp);
+            acc = __dsub_rn(acc, zm[i]);
+            acc = __dsub_rn(acc, zp[i]);
+            res = __dsub_rn(fv, acc);
+          } else {
+            res = residual7(st, fv, c[i], xl, xr, ym, yp, zm[i], zp[i]);
+          }
+          ssq = fma(res, res, ssq);
+          rb[row * RS + x + (x >> 5)] = res;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+    if (lane == 0) wsum[b * C::AC_WARPS + warp] = ssq;
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty_u[s_cur]);
+      mbar_arrive(&empty_f[t]);
+    }
+    named_arrive(kBarR + b, NBAR);
+    if (k > k0) phaseC<FULL>(zm);  // u(k-1) is this plane's zm
+    vbase_old = (long long)(k + 1) * pxy + (long long)(j0 + 1) * PX + 1;
+    s_cur = s_nxt;
+    b ^= 1;
+  }
+
+  template <bool FULL>
+  __device__ __forceinline__ void run_unit(int ka, int kb) {
+    {  // slab ka-1 -> A0
+      const int sidx = nu % C::NU;
+      mbar_wait(&full_u[sidx], (nu / C::NU) & 1);
+      load_c(A0, uring + sidx * C::US);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_u[sidx]);
+      ++nu;
+    }
+    s_cur = nu % C::NU;  // slab ka -> A1, slot kept for the halo rows
+    mbar_wait(&full_u[s_cur], (nu / C::NU) & 1);
+    ++nu;
+    load_c(A1, uring + s_cur * C::US);
+    int k = ka;
+    for (;;) {
+      step<FULL>(A0, A1, A2, k++);
+      if (k >= kb) { phaseC<FULL>(A1); break; }
+      step<FULL>(A1, A2, A0, k++);
+      if (k >= kb) { phaseC<FULL>(A2); break; }
+      step<FULL>(A2, A0, A1, k++);
+      if (k >= kb) { phaseC<FULL>(A0); break; }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_u[s_cur]);  // the unit's last slab (plane kb)
+  }
+};
+
 template <int NX, int UNIT>
 __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
     line_jacobi_zmarch_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
                               StencilDev st, double omega, double* __restrict__ partials,
-                              const ZUnit* __restrict__ units, int nunits) {
+                              const ZUnit* __restrict__ units, int nunits, const __grid_constant__ ZTab T) {
   using C = ZCfg<NX>;
   constexpr int R = C::R, PX = C::PX, NSEG = C::NSEG, NSL = C::NSL, RS = C::RS, E = C::E, ACT = C::ACT;
   extern __shared__ __align__(128) double zsm[];
   double* uring = zsm;
   double* fring = uring + C::NU * C::US;
   double* rbuf = fring + C::NF * C::FS;
-  double* clb = rbuf + 2 * C::RB;
-  double* crb = clb + 2 * NSL;
-  double* wsum = crb + 2 * NSL;
-  double* tab = wsum + 2 * C::AC_WARPS;  // invm, loinv, cp, g, h, g16|h16
-  uint64_t* bars = (uint64_t*)(tab + 7 * kSeg);
+  double* wsum = rbuf + 2 * C::RB;
+  uint64_t* bars = (uint64_t*)(wsum + 2 * C::AC_WARPS);
   uint64_t* full_u = bars;
   uint64_t* empty_u = full_u + C::NU;
   uint64_t* full_f = empty_u + C::NU;
@@ -139,19 +292,6 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
       mbar_init(&empty_f[s], C::AC_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // factor tables: every patch of one launch shares nx and the stencil, so
-  // the first unit's LineFac serves all (psm_api.cu groups launches by nx)
-  if (tid < kSeg && nunits > 0) {
-    const LineFac* L = patches[units[0].patch].lf;
-    const double im = L->invm[tid];
-    tab[tid] = im;
-    tab[kSeg + tid] = L->lo * im;
-    tab[2 * kSeg + tid] = L->cp[tid];
-    tab[3 * kSeg + tid] = L->g[tid];
-    tab[4 * kSeg + tid] = L->h[tid];
-    tab[5 * kSeg + tid] = L->g16[tid & 15];  // [5k..5k+15] g16, [5k+16..] h16
-    if (tid >= 16) tab[5 * kSeg + tid] = L->h16[tid - 16];
   }
   __syncthreads();
 
@@ -192,9 +332,8 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
   if (warp >= C::AC_WARPS) {
     const int sl = tid - C::AC_WARPS * 32;  // 0..NSL-1
     const int r = sl / NSEG, s = sl % NSEG;
-    const LineFac* L = patches[units[0].patch].lf;
-    const double lo = L->lo, up = L->up, up_h31 = L->up_h31, lo_g0 = L->lo_g0, d_full = L->d_full;
-    const double up_h16 = L->up_h16, lo_g16 = L->lo_g16, d16 = L->d16;
+    const double lo = T.lo, up = T.up, up_h31 = T.up_h31, lo_g0 = T.lo_g0, d_full = T.d_full;
+    const double up_h16 = T.up_h16, lo_g16 = T.lo_g16, d16 = T.d16;
     int b = 0;
     for (int w = blockIdx.x; w < nunits; w += gridDim.x) {
       const ZUnit U = units[w];
@@ -213,18 +352,18 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
         double ya[16], yb[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          ya[i] = seg[i] * tab[i];
-          yb[i] = seg[16 + i] * tab[i];
+          ya[i] = seg[i] * T.invm[i];
+          yb[i] = seg[16 + i] * T.invm[i];
         }
 #pragma unroll
         for (int i = 1; i < 16; ++i) {
-          ya[i] = fma(-tab[kSeg + i], ya[i - 1], ya[i]);
-          yb[i] = fma(-tab[kSeg + i], yb[i - 1], yb[i]);
+          ya[i] = fma(-T.loinv[i], ya[i - 1], ya[i]);
+          yb[i] = fma(-T.loinv[i], yb[i - 1], yb[i]);
         }
 #pragma unroll
         for (int i = 14; i >= 0; --i) {
-          ya[i] = fma(-tab[2 * kSeg + i], ya[i + 1], ya[i]);
-          yb[i] = fma(-tab[2 * kSeg + i], yb[i + 1], yb[i]);
+          ya[i] = fma(-T.cp[i], ya[i + 1], ya[i]);
+          yb[i] = fma(-T.cp[i], yb[i + 1], yb[i]);
         }
         const double xa15 = (ya[15] - up_h16 * yb[0]) * d16;
         const double xb0 = yb[0] - lo_g16 * xa15;
@@ -232,20 +371,19 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
         double yv[kSeg];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          yv[i] = fma(-ca, tab[5 * kSeg + 16 + i], ya[i]);
-          yv[16 + i] = fma(-cb, tab[5 * kSeg + i], yb[i]);
+          yv[i] = fma(-ca, T.h16[i], ya[i]);
+          yv[16 + i] = fma(-cb, T.g16[i], yb[i]);
         }
         const double ylast = yv[kSeg - 1];
-#pragma unroll
-        for (int i = 0; i < kSeg; ++i) seg[i] = yv[i];
         const double yfirst = yv[0];
         const double yl_left = __shfl_up_sync(0xffffffffu, ylast, 1);
         const double yf_right = __shfl_down_sync(0xffffffffu, yfirst, 1);
         double clv = 0.0, crv = 0.0;
         if (s > 0) clv = lo * ((yl_left - up_h31 * yfirst) * d_full);
         if (s < NSEG - 1) crv = up * (yf_right - lo_g0 * ((ylast - up_h31 * yf_right) * d_full));
-        clb[b * NSL + sl] = clv;
-        crb[b * NSL + sl] = crv;
+        // exact solution of the segment: y - lo*x_left*g - up*x_right*h
+#pragma unroll
+        for (int i = 0; i < kSeg; ++i) seg[i] = fma(-crv, T.h[i], fma(-clv, T.g[i], yv[i]));
         named_arrive(kBarY + b, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
       }
     }
@@ -253,145 +391,41 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
   }
 
   // ======================= A/C warps =========================================
-  const double* tg = tab + 3 * kSeg;
-  const double* th = tab + 4 * kSeg;
-  const double tgl = tg[lane], thl = th[lane];
-  uint32_t nu = 0, nf = 0;
-  int b = 0;
+  ZAC<NX, UNIT> ac;
+  ac.tid = tid;
+  ac.lane = lane;
+  ac.warp = warp;
+  ac.st = st;
+  ac.omega = omega;
+  ac.uring = uring;
+  ac.fring = fring;
+  ac.rbuf = rbuf;
+  ac.wsum = wsum;
+  ac.full_u = full_u;
+  ac.empty_u = empty_u;
+  ac.full_f = full_f;
+  ac.empty_f = empty_f;
+  ac.tx = ZAC<NX, UNIT>::NX_GE ? tid : tid % NX;
+  ac.trow0 = ZAC<NX, UNIT>::NX_GE ? 0 : (tid / NX) * ZAC<NX, UNIT>::RPT;
   for (int w = blockIdx.x; w < nunits; w += gridDim.x) {
     const ZUnit U = units[w];
     const PatchDev& P = patches[U.patch];
-    const int rows = min(R, P.ny - U.j0);
-    const long long pxy = (long long)PX * (P.ny + 2);
-    double* v = P.buf[active[U.patch] ^ 1];
-    double zm[E], c[E], zp[E], cold[E];
-    long long vbase_old = 0;
-    // slab k0-1 -> zm
-    {
-      const int s = nu % C::NU;
-      mbar_wait(&full_u[s], (nu / C::NU) & 1);
-      const double* sl = uring + s * C::US;
-#pragma unroll
-      for (int q = 0; q < E; ++q) zm[q] = sl[(cell_row<NX, ACT>(q, tid) + 1) * PX + cell_x<NX, ACT>(q, tid) + 1];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_u[s]);
-      ++nu;
-    }
-    // slab k0 -> c (slot kept for the y-neighbours)
-    int s_cur = nu % C::NU;
-    mbar_wait(&full_u[s_cur], (nu / C::NU) & 1);
-    ++nu;
-    {
-      const double* sl = uring + s_cur * C::US;
-#pragma unroll
-      for (int q = 0; q < E; ++q) c[q] = sl[(cell_row<NX, ACT>(q, tid) + 1) * PX + cell_x<NX, ACT>(q, tid) + 1];
-    }
-    // C: x = y - cl*g - cr*h, v = u + omega*x (previous plane's buffers)
-    auto phaseC = [&](auto full_t) {
-      constexpr bool FULL = decltype(full_t)::value;
-      const int bo = b ^ 1;
-      named_sync(kBarY + bo, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
-      const double* yb = rbuf + bo * C::RB;
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const int row = cell_row<NX, ACT>(q, tid), x = cell_x<NX, ACT>(q, tid);
-        if (FULL || row < rows) {
-          const int sg = row * NSEG + (x >> 5);
-          const double xs = fma(-crb[bo * NSL + sg], thl, fma(-clb[bo * NSL + sg], tgl, yb[row * RS + x + (x >> 5)]));
-          const double nv = relax(cold[q], omega, xs);
-          const long long iu = vbase_old + (long long)row * PX + x;
-          v[iu] = nv;
-          if constexpr (NX >= ACT) {
-            if ((q * ACT) % NX == 0 && tid == 0) v[iu - 1] = -nv;
-            if ((q * ACT) % NX == NX - ACT && tid == ACT - 1) v[iu + 1] = -nv;
-          } else {
-            if (x == 0) v[iu - 1] = -nv;
-            if (x == NX - 1) v[iu + 1] = -nv;
-          }
-        }
-      }
-    };
-    // A: residual of plane k
-    auto phaseA = [&](auto full_t, const double* cur, const double* nxt, const double* fs, double* rb) {
-      constexpr bool FULL = decltype(full_t)::value;
-      double ssq = 0.0;
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const int row = cell_row<NX, ACT>(q, tid), x = cell_x<NX, ACT>(q, tid);
-        zp[q] = nxt[(row + 1) * PX + x + 1];
-        double xl = __shfl_up_sync(0xffffffffu, c[q], 1);
-        double xr = __shfl_down_sync(0xffffffffu, c[q], 1);
-        if (lane == 0) xl = cur[(row + 1) * PX + x];
-        if (lane == 31) xr = cur[(row + 1) * PX + x + 2];
-        if (FULL || row < rows) {
-          const double ym = cur[row * PX + x + 1];
-          const double yp = cur[(row + 2) * PX + x + 1];
-          const double fv = fs[row * NX + x];
-          double res;
-          if (UNIT) {
-            double acc = __dmul_rn(st.c, c[q]);
-            acc = __dsub_rn(acc, xl);
-            acc = __dsub_rn(acc, xr);
-            acc = __dsub_rn(acc, ym);
-            acc = __dsub_rn(acc, yp);
-            acc = __dsub_rn(acc, zm[q]);
-            acc = __dsub_rn(acc, zp[q]);
-            res = __dsub_rn(fv, acc);
-          } else {
-            res = residual7(st, fv, c[q], xl, xr, ym, yp, zm[q], zp[q]);
-          }
-          ssq = fma(res, res, ssq);
-          rb[row * RS + x + (x >> 5)] = res;
-        }
-      }
-      return ssq;
-    };
-    const bool full = rows == R;
-    for (int k = U.k0; k < U.k1; ++k) {
-      const int s_nxt = nu % C::NU;
-      mbar_wait(&full_u[s_nxt], (nu / C::NU) & 1);
-      ++nu;
-      const int t = nf % C::NF;
-      mbar_wait(&full_f[t], (nf / C::NF) & 1);
-      ++nf;
-      const double* cur = uring + s_cur * C::US;
-      const double* nxt = uring + s_nxt * C::US;
-      const double* fs = fring + t * C::FS;
-      double* rb = rbuf + b * C::RB;
-      double ssq = full ? phaseA(std::true_type{}, cur, nxt, fs, rb) : phaseA(std::false_type{}, cur, nxt, fs, rb);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
-      if (lane == 0) wsum[b * C::AC_WARPS + warp] = ssq;
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty_u[s_cur]);
-        mbar_arrive(&empty_f[t]);
-      }
-      named_arrive(kBarR + b, (C::AC_WARPS + C::SOLVER_WARPS) * 32);
-      if (k > U.k0) {
-        if (full) phaseC(std::true_type{}); else phaseC(std::false_type{});
-      }
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        cold[q] = c[q];
-        zm[q] = c[q];
-        c[q] = zp[q];
-      }
-      vbase_old = (long long)(k + 1) * pxy + (long long)(U.j0 + 1) * PX + 1;
-      s_cur = s_nxt;
-      b ^= 1;
-    }
-    // the unit's last slab (plane k1) is done; C of its last plane
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_u[s_cur]);
-    if (full) phaseC(std::true_type{}); else phaseC(std::false_type{});
+    ac.rows = min(R, P.ny - U.j0);
+    ac.pxy = (long long)PX * (P.ny + 2);
+    ac.v = P.buf[active[U.patch] ^ 1];
+    ac.j0 = U.j0;
+    ac.k0 = U.k0;
+    if (ac.rows == R)
+      ac.template run_unit<true>(U.k0, U.k1);
+    else
+      ac.template run_unit<false>(U.k0, U.k1);
   }
 }
 
 template <int NX>
 static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                            double omega, double* partials, const ZUnit* units, int nunits, int grid,
-                           cudaStream_t stream) {
+                           const ZTab& T, cudaStream_t stream) {
   using C = ZCfg<NX>;
   static bool attr = false;
   if (!attr) {
@@ -403,10 +437,10 @@ static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned cha
   }
   if (unit)
     line_jacobi_zmarch_kernel<NX, 1><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega,
-                                                                                  partials, units, nunits);
+                                                                                  partials, units, nunits, T);
   else
     line_jacobi_zmarch_kernel<NX, 0><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega,
-                                                                                  partials, units, nunits);
+                                                                                  partials, units, nunits, T);
   return cudaGetLastError();
 }
 
@@ -414,16 +448,36 @@ int zmarch_rows(int nx) { return kMaxTileCells / nx; }
 
 cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
                                const StencilDev& st, double omega, double* partials, const void* units, int nunits,
-                               int grid, cudaStream_t stream) {
+                               int grid, const LineFac& L, cudaStream_t stream) {
   if (nunits <= 0) return cudaSuccess;
   if (grid > nunits) grid = nunits;
   const ZUnit* u = (const ZUnit*)units;
+  ZTab T;
+  for (int i = 0; i < kSeg; ++i) {
+    T.invm[i] = L.invm[i];
+    T.loinv[i] = L.lo * L.invm[i];
+    T.cp[i] = L.cp[i];
+    T.g[i] = L.g[i];
+    T.h[i] = L.h[i];
+  }
+  for (int i = 0; i < 16; ++i) {
+    T.g16[i] = L.g16[i];
+    T.h16[i] = L.h16[i];
+  }
+  T.lo = L.lo;
+  T.up = L.up;
+  T.up_h31 = L.up_h31;
+  T.lo_g0 = L.lo_g0;
+  T.d_full = L.d_full;
+  T.up_h16 = L.up_h16;
+  T.lo_g16 = L.lo_g16;
+  T.d16 = L.d16;
   switch (nx) {
-    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
-    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
-    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
-    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
-    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, stream);
+    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
+    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
+    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
+    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
+    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
     default: return cudaErrorInvalidValue;
   }
 }
