@@ -339,7 +339,7 @@ def run_ours(args, rank, world, local_rank):
         "unit": "GB/s",
         "frac": achieved / peak,
         "traffic": _traffic(f"line_jacobi_{nx}x{ny}x{p.dims.nz}"),
-        "kernel": "psm::line_tile_kernel<1> (line Jacobi sweep, fused residual norm + x ghosts)",
+        "kernel": f"psm::line_jacobi_zmarch_kernel<{nx},1> (line Jacobi sweep, fused residual norm + x ghosts)",
         "bytes_per_launch": BYTES_PER_UPDATE * local_cells,
         "avg_launch_ms": sweep_ms,
         "peak_source": peak_src,
