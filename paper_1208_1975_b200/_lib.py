@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsmooth.so")
+LIB_PATH = os.environ.get("PSM_LIB", os.path.join(_HERE, "libpsmooth.so"))  # override: tools/profiling builds
 
 PSM_OK = 0
 PSM_EINVAL = -1

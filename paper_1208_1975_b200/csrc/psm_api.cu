@@ -78,6 +78,12 @@ int psm_plane_plan_setup(psm_plan* plan);  // psm_plane.cu
 int psm_plane_plan_free(psm_plan* plan);
 int psm_plane_jacobi(psm_plan* P, const unsigned char* d_active, double omega, double* partials, cudaStream_t s);
 int psm_plane_gs(psm_plan* P, const unsigned char* d_active, double omega, cudaStream_t s);
+// pipelined line GS (psm_line_gs_pipe.cu)
+bool gs_pipe_supported(int nx);
+int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets);
+void psm_gs_pipe_free(psm_plan* P);
+int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int chaotic, int* flags, int* tickets,
+                      cudaStream_t s);
 
 int psm_set_error(int code, const char* msg) {
   g_err = msg;
@@ -390,6 +396,8 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_flags);
   cudaFree(P->d_unit_patch);
   cudaFree(P->d_unit_plane);
+  cudaFree(P->d_gsflags);
+  psm_gs_pipe_free(P);
   for (auto& kv : P->unit_cache) cudaFree(kv.second.first);
   for (auto& kv : P->active_cache) cudaFree(kv.second);
   if (P->kind == PSM_BLOCK_PLANE) psm_plane_plan_free(P);
@@ -660,6 +668,20 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
   cudaStream_t s = (cudaStream_t)stream;
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_gs(P, da, omega, s);
   if (P->kind != PSM_BLOCK_LINE) return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
+  bool pipe = true;
+  for (auto& h : P->hp)  // TMA row copies need 16-byte aligned buffers
+    pipe = pipe && gs_pipe_supported(h.nx) && (((uintptr_t)h.buf[0] | (uintptr_t)h.buf[1]) % 16 == 0);
+  if (pipe) {
+    if (!P->gspipe) {
+      int nt = 0;
+      rc = psm_gs_pipe_prepare(P, &nt);
+      if (rc) return rc;
+      P->gs_ntickets = nt;
+      CUDA_TRY(cudaMalloc(&P->d_gsflags, (P->nplanes + nt) * sizeof(int)));
+    }
+    CUDA_TRY(cudaMemsetAsync(P->d_gsflags, 0, (P->nplanes + P->gs_ntickets) * sizeof(int), s));
+    return psm_gs_pipe_sweep(P, da, omega, mode == PSM_GS_CHAOTIC, P->d_gsflags, P->d_gsflags + P->nplanes, s);
+  }
   int max_nx = 0;
   for (auto& h : P->hp) max_nx = std::max(max_nx, h.nx);
   if (!P->tiled || gs_chunks_for(max_nx) == 0) {

@@ -119,6 +119,7 @@ constexpr int kMaxTileCells = 2048;  // cells per line tile (8 per thread at 256
 #include <vector>
 
 struct PlaneState;  // psm_plane.cu
+struct GsPipeState;  // psm_line_gs_pipe.cu
 
 struct psm_factors {
   // host handle for one block shape
@@ -163,6 +164,10 @@ struct psm_plan {
   long long launches = 0;  // kernels this plan launched (bench evidence)
   std::map<int, int> nx_grid;  // persistent grid per specialised nx
   std::map<std::string, std::pair<void*, int>> unit_cache;  // z-marching units per plane range
+  // pipelined line GS (psm_line_gs_pipe.cu)
+  GsPipeState* gspipe = nullptr;
+  int* d_gsflags = nullptr;  // nplanes progress words + one ticket per group
+  int gs_ntickets = 0;
   // plane path
   PlaneState* plane = nullptr;
 };

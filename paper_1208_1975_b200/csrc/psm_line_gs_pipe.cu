@@ -1,0 +1,681 @@
+// Line-block Gauss-Seidel, plane-pipelined CTAs with warp-level PCR solves.
+//
+// Replaces smoother._gs_step + block_residual + block_update/matvec for line
+// blocks (smoother.py:156-169, stencil.py:93-112, blocklinalg.py:90-105) when
+// nx is 32, 64, 128 or 256.  Ghosts are lagged until the step-end refresh,
+// as in the reference.
+//
+// Order.  The serial strategy visits x-lines (j,k) of a patch
+// lexicographically, j fastest (runtime.py:164-168): line (j,k) reads the NEW
+// lines (j-1,k) and (j,k-1) and the OLD lines (j+1,k), (j,k+1).  Here a work
+// unit is W consecutive planes k0..k0+W-1 of one patch; warp w of the CTA owns
+// plane k0+w and walks its rows j = 0..ny-1 in order.  Row j of plane k waits
+// for row j of plane k-1 (previous warp: shared-memory progress counter and a
+// ring of new rows; previous CTA: a global acquire/release flag), so every
+// line computes exactly the lexicographic arithmetic: a wavefront schedule over
+// d = j + k.  CHAOTIC drops the acquire/release ordering on the cross-CTA flag
+// (relaxed accesses, no fences): in-place block updates without a global
+// memory ordering, the contract of smooth_chaotic_gs_step under parallel
+// strategies.
+//
+// Line solve.  Lane L owns the NC = nx/32 contiguous cells L*NC .. L*NC+NC-1.
+// Cells 0..NC-2 of a chunk are eliminated locally (constant Thomas factors and
+// spikes g, h: one set serves every chunk), which leaves one tridiagonal
+// interface system in the chunks' last cells a_L.  That 32-unknown system is
+// solved exactly by five parallel-cyclic-reduction steps over warp shuffles
+// with per-lane coefficients built once on the host in long double.  The
+// chunk cells then follow as x = y - a_{L-1} g - a_L h.
+//
+// Data movement.  Per row a lane issues 8-byte cp.async copies (coalesced on
+// the global side) of the old rows u(j+1,k), u(j,k+1), f(j,k) and the row's two
+// x-ghosts into a 3-deep per-warp ring, two rows ahead of use; the shared
+// layout pos(x) = (x % NC)*(32 + 16/NC) + x/NC makes both the coalesced copy
+// and the lane-chunk reads bank-conflict free.  New rows go through a 2-deep
+// per-warp ring: it feeds the next warp's u(j,k-1) and the coalesced global
+// store of the row.
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "psm_internal.cuh"
+
+namespace psm {
+
+constexpr int kGsW = 7;       // planes (compute warps) per CTA unit; + 1 publisher warp
+constexpr int kGsThreads = (kGsW + 1) * 32;
+constexpr int kGsTab = 18;    // per-lane table entries: q0,q1,q2 + 5 PCR steps x (p0,p1,p2)
+constexpr int kGsPub = 4;     // wavefront mode: rows per release of the cross-CTA flag
+
+// uniform chunk-interior tables (passed by value: constant-bank operands)
+struct GsUniform {
+  double invm[8], loinv[8], cp[8], g[8], h[8];
+  int npcr;  // PCR steps until the remaining interface couplings are < 1e-20 (<= 5: exact)
+};
+
+template <int NC>
+struct GCfg {
+  static constexpr int IS = 32 + 16 / NC;      // stride between the NC "i-rows" of a slot
+  static constexpr int SLOT = NC * IS + 2;     // doubles per ring slot (+ the two x-ghosts)
+  static constexpr int D = 3;                  // prefetch ring depth
+  static constexpr int P = D - 1;              // rows of prefetch ahead
+  static constexpr int DH = 2;                 // new-row ring depth (warp -> next warp)
+  static constexpr int DHL = 4;                // new-row ring depth (last warp -> publisher)
+  static constexpr int DM = 3;                 // warp 0: rows of plane k0-1 in flight (TMA)
+  static constexpr int MROW = 32 * NC + 2;     // padded row, contiguous
+  static constexpr int NBAR = 2 * kGsW * DH + 2 * DHL + DM;  // mbarriers
+  static constexpr int HEAD_DOUBLES = kGsTab * 32 + 8 + NBAR + (NBAR & 1);  // tables, ints, mbarriers
+  static constexpr int WARP_DOUBLES = (3 * D + DH) * SLOT;
+  static constexpr int LAST_DOUBLES = (3 * D + DHL) * SLOT;
+  // warp 0's ring: the lagged ghost plane u(j,-1) when k0 == 0 (cp.async,
+  // chunk layout), else the new rows of plane k0-1 (TMA bulk, padded rows)
+  static constexpr int MR = (D * SLOT > DM * MROW) ? D * SLOT : DM * MROW;
+  static constexpr size_t SMEM =
+      (size_t)(HEAD_DOUBLES + (kGsW - 1) * WARP_DOUBLES + LAST_DOUBLES + MR) * sizeof(double);
+  static constexpr int MINB = NC >= 8 ? 1 : 2;
+  __device__ static __forceinline__ int pos(int x) { return (x % NC) * IS + x / NC; }
+};
+
+__device__ __forceinline__ uint32_t sm32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sm32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Deadlock guard for the progress spins: trap (a launch error, not a hung
+// GPU) if one wait exceeds ~2^35 cycles (~17 s).
+__device__ __forceinline__ long long clk64() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+struct SpinGuard {
+  long long t0;
+  __device__ __forceinline__ SpinGuard() : t0(clk64()) {}
+  __device__ __forceinline__ void check() {
+    if (clk64() - t0 > (1LL << 35)) __trap();
+  }
+};
+
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void gs_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void gs_mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(sm32(bar)) : "memory");
+}
+__device__ __forceinline__ void gs_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm32(bar)) : "memory");
+}
+__device__ __forceinline__ void gs_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void gs_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "GMBW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra GMBW_%=;\n"
+      "}\n" ::"r"(sm32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void gs_tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm32(dst)),
+      "l"(src), "r"(bytes), "r"(sm32(bar))
+      : "memory");
+}
+
+#ifdef PSM_GS_PROFILE
+// phase timing of block 0, warp 0, lane 0 (tools/gs_phase_probe.py)
+__device__ long long g_gs_prof[16];
+#define GS_PROF(ph, dep)                                                   \
+  do {                                                                     \
+    if (prof_on) {                                                         \
+      double _t;                                                           \
+      asm volatile("mov.b64 %0, %1;" : "=d"(_t) : "d"((double)(dep)));     \
+      (void)_t;                                                            \
+      const long long _c = clk64();                                        \
+      g_gs_prof[ph] += _c - prof_t;                                        \
+      prof_t = _c;                                                         \
+    }                                                                      \
+  } while (0)
+#else
+#define GS_PROF(ph, dep) \
+  do {                   \
+  } while (0)
+#endif
+
+template <int NC, int CHAOTIC, int UNIT>
+__global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
+    line_gs_pipe_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
+                        StencilDev st, double omega, int* __restrict__ flags, int* __restrict__ ticket,
+                        const int2* __restrict__ units, int nunits, const double* __restrict__ lane_tab,
+                        const __grid_constant__ GsUniform T) {
+  using C = GCfg<NC>;
+  constexpr int M = NC - 1;  // locally eliminated cells per chunk
+  constexpr int nx = 32 * NC;
+  constexpr int IS = C::IS, SLOT = C::SLOT, D = C::D, P = C::P, DH = C::DH, DHL = C::DHL, DM = C::DM;
+  constexpr int MROW = C::MROW;
+  extern __shared__ __align__(16) double gsm[];
+  double* tab = gsm;                                   // [kGsTab][32]
+  int* unit_sh = (int*)(gsm + kGsTab * 32);            // current unit
+  uint64_t* bars = (uint64_t*)(gsm + kGsTab * 32 + 8);
+  uint64_t* fullH = bars;                              // [kGsW][DH] warp w -> warp w+1
+  uint64_t* emptyH = fullH + kGsW * DH;
+  uint64_t* fullL = emptyH + kGsW * DH;                // [DHL] last warp -> publisher
+  uint64_t* emptyL = fullL + DHL;
+  uint64_t* mbarM = emptyL + DHL;                      // [DM] warp 0's TMA rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = gsm + C::HEAD_DOUBLES;
+  double* Ur = ring + warp * C::WARP_DOUBLES;          // old u(j+1,k) + x-ghosts of row j
+  double* Zr = Ur + D * SLOT;                          // old u(j,k+1)
+  double* Fr = Zr + D * SLOT;                          // f(j,k)
+  double* Hr = Fr + D * SLOT;                          // new u(j,k)
+  double* HL = ring + (kGsW - 1) * C::WARP_DOUBLES + 3 * D * SLOT;  // last warp's new rows (DHL)
+  const double* Hprev = Hr - C::WARP_DOUBLES;          // previous warp's new rows
+  double* Mr = ring + (kGsW - 1) * C::WARP_DOUBLES + C::LAST_DOUBLES;
+  uint32_t mbase = 0;  // warp 0: TMA row loads completed in earlier units
+
+  for (int e = threadIdx.x; e < kGsTab * 32; e += blockDim.x) tab[e] = lane_tab[e];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < DM; ++i) gs_mbar_init(&mbarM[i], 1);
+  }
+  __syncthreads();
+  const double* q = tab + lane;  // q[32*e]: this lane's table entry e
+  int dpos[NC];  // shared-memory position of this lane's coalesced cell i*32+lane
+#pragma unroll
+  for (int i = 0; i < NC; ++i) dpos[i] = C::pos(i * 32 + lane);
+
+  for (int first = 1;; first = 0) {
+    if (threadIdx.x == 0) {
+      unit_sh[0] = atomicAdd(ticket, 1);
+      for (int i = 0; i < 2 * kGsW * DH + 2 * DHL; ++i) {
+        if (!first) gs_mbar_inval(&bars[i]);
+        gs_mbar_init(&bars[i], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int u = unit_sh[0];
+    if (u >= nunits) return;
+    const int2 U = units[u];
+    const PatchDev& Pd = patches[U.x];
+    const int nz = Pd.nz, ny = Pd.ny;
+    const long long px = nx + 2, pxy = px * (ny + 2);
+    double* Ub = Pd.buf[active[U.x]];
+
+    if (warp == kGsW) {
+      // ======================= publisher ====================================
+      const int kl = U.y + kGsW - 1;  // plane of the last compute warp
+      if (kl < nz) {
+        double* row0 = Ub + (long long)(kl + 1) * pxy + px + 1;
+        int* my_flag = flags + Pd.plane0 + kl;
+        const bool succ = kl + 1 < nz;
+        for (int j = 0; j < ny; ++j) {
+          const int s = j % DHL;
+          gs_mbar_wait(&fullL[s], (j / DHL) & 1);
+          const double* hs = HL + s * SLOT;
+          double* dst = row0 + (long long)j * px;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) __stcg(dst + i * 32 + lane, hs[dpos[i]]);
+          __syncwarp();
+          if (lane == 0) {
+            gs_mbar_arrive(&emptyL[s]);
+            if (succ) {
+              // release: cumulative over the warp's stores (warp barrier above)
+              if (CHAOTIC) st_relaxed_gpu(my_flag, j + 1);
+              else if ((j + 1) % kGsPub == 0 || j == ny - 1) st_release_gpu(my_flag, j + 1);
+            }
+          }
+        }
+      }
+    } else if (U.y + warp < nz) {
+      // ======================= compute warp: plane k ========================
+      const int k = U.y + warp;
+      const bool last = warp == kGsW - 1;
+      const bool consumer = !last && (k + 1 < nz);
+      double* row0 = Ub + (long long)(k + 1) * pxy + px + 1;  // u(0, 0, k)
+      const double* Fk = Pd.f + (long long)k * ny * nx;
+      const int* dep_flag = flags + Pd.plane0 + k - 1;
+
+      auto issue = [&](int j) {
+        if (j < ny) {
+          const int s = (j % D) * SLOT;
+          const double* src_u = row0 + (long long)(j + 1) * px;
+          const double* src_z = src_u - px + pxy;
+          const double* src_f = Fk + (long long)j * nx;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) {
+            const int x = i * 32 + lane;
+            cp_async8(Ur + s + dpos[i], src_u + x);
+            cp_async8(Zr + s + dpos[i], src_z + x);
+            cp_async8(Fr + s + dpos[i], src_f + x);
+          }
+          if (warp == 0 && k == 0) {
+            const double* src_m = src_u - px - pxy;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) cp_async8(Mr + s + dpos[i], src_m + i * 32 + lane);
+          }
+          if (lane < 2) cp_async8(Ur + s + NC * IS + lane, src_u - px + (lane ? nx : -1));
+        }
+        cp_commit();
+      };
+
+      double cen[NC], ym[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        cen[i] = row0[lane * NC + i];
+        ym[i] = row0[lane * NC + i - px];
+      }
+#pragma unroll
+      for (int j = 0; j < P; ++j) issue(j);
+      int avail = 0, issued = 0;  // warp 0, k > 0: rows of plane k-1 published / requested
+
+#ifdef PSM_GS_PROFILE
+      const bool prof_on = blockIdx.x == 0 && warp == 0 && lane == 0;
+      long long prof_t = clk64();
+#endif
+      for (int j = 0; j < ny; ++j) {
+        GS_PROF(0, 0.0);
+        issue(j + P);
+        GS_PROF(1, 0.0);
+        cp_wait<P>();
+        __syncwarp();
+        GS_PROF(2, 0.0);
+        const int s = (j % D) * SLOT;
+        double nxt[NC], zp[NC], fv[NC], zm[NC];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          nxt[i] = Ur[s + i * IS + lane];
+          zp[i] = Zr[s + i * IS + lane];
+          fv[i] = Fr[s + i * IS + lane];
+        }
+        const double gl = Ur[s + NC * IS], gr = Ur[s + NC * IS + 1];
+        // ---- u(j, k-1), new ----------------------------------------------
+        if (warp > 0) {
+          const int hs = j % DH;
+          gs_mbar_wait(&fullH[(warp - 1) * DH + hs], (j / DH) & 1);
+          const double* h = Hprev + hs * SLOT;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) zm[i] = h[i * IS + lane];
+          __syncwarp();
+          if (lane == 0) gs_mbar_arrive(&emptyH[(warp - 1) * DH + hs]);
+        } else if (k == 0) {
+#pragma unroll
+          for (int i = 0; i < NC; ++i) zm[i] = Mr[s + i * IS + lane];
+        } else {
+          // new rows of plane k0-1 (previous CTA's publisher): TMA bulk copies
+          // through L2 (never a stale L1 line), issued once published
+          if (lane == 0) {
+            if (avail <= j) {
+              SpinGuard sg;
+              while ((avail = ld_relaxed_gpu(dep_flag)) <= j) sg.check();
+              if (!CHAOTIC) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            const int lim = min(avail, j + DM);
+            for (; issued < lim; ++issued) {
+              const uint32_t n = mbase + (uint32_t)issued;
+              gs_mbar_expect_tx(&mbarM[n % DM], MROW * 8);
+              gs_tma_row(Mr + (n % DM) * MROW, row0 + (long long)issued * px - pxy - 1, MROW * 8, &mbarM[n % DM]);
+            }
+          }
+          __syncwarp();
+          const uint32_t n = mbase + (uint32_t)j;
+          gs_mbar_wait(&mbarM[n % DM], (n / DM) & 1);
+          const double* mrow = Mr + (n % DM) * MROW + 1 + lane * NC;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) zm[i] = mrow[i];
+        }
+        GS_PROF(3, zm[NC - 1] + fv[NC - 1] + nxt[NC - 1] + zp[NC - 1]);
+        // ---- residual in the reference operation order ------------------
+        double r[NC];
+        {
+          const double lft = __shfl_up_sync(0xffffffffu, cen[NC - 1], 1);
+          const double rgt = __shfl_down_sync(0xffffffffu, cen[0], 1);
+#pragma unroll
+          for (int i = 0; i < NC; ++i) {
+            const double xl = i > 0 ? cen[i > 0 ? i - 1 : 0] : (lane == 0 ? gl : lft);
+            const double xr = i < NC - 1 ? cen[i < NC - 1 ? i + 1 : 0] : (lane == 31 ? gr : rgt);
+            if (UNIT) {  // faces all -1: face*nbr is exactly -nbr, same roundings
+              double acc = __dmul_rn(st.c, cen[i]);
+              acc = __dsub_rn(acc, xl);
+              acc = __dsub_rn(acc, xr);
+              acc = __dsub_rn(acc, ym[i]);
+              acc = __dsub_rn(acc, nxt[i]);
+              acc = __dsub_rn(acc, zm[i]);
+              acc = __dsub_rn(acc, zp[i]);
+              r[i] = __dsub_rn(fv[i], acc);
+            } else {
+              r[i] = residual7(st, fv[i], cen[i], xl, xr, ym[i], nxt[i], zm[i], zp[i]);
+            }
+          }
+        }
+        GS_PROF(4, r[NC - 1] + r[0]);
+        // ---- exact line solve: local elimination + PCR ------------------
+        double y[NC];
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          y[i] = i == 0 ? r[0] * T.invm[0] : fma(-T.loinv[i], y[i > 0 ? i - 1 : 0], r[i] * T.invm[i]);
+#pragma unroll
+        for (int i = M - 2; i >= 0; --i) y[i] = fma(-T.cp[i], y[i + 1], y[i]);
+        GS_PROF(5, y[0] + y[M > 0 ? M - 1 : 0]);
+        double rho = q[0] * r[NC - 1];
+        if (M > 0) {
+          const double y0r = __shfl_down_sync(0xffffffffu, y[0], 1);
+          rho = fma(-q[32], y[M > 0 ? M - 1 : 0], rho);
+          rho = fma(-q[64], y0r, rho);
+        }
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          if (t < T.npcr) {
+            const int dd = 1 << t;
+            const double rl = __shfl_up_sync(0xffffffffu, rho, dd);
+            const double rr = __shfl_down_sync(0xffffffffu, rho, dd);
+            rho = fma(-q[32 * (5 + 3 * t)], rr, fma(-q[32 * (4 + 3 * t)], rl, q[32 * (3 + 3 * t)] * rho));
+          }
+        }
+        GS_PROF(6, rho);
+        double al = __shfl_up_sync(0xffffffffu, rho, 1);
+        if (lane == 0) al = 0.0;
+        double nv[NC];
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          const double xv = i < M ? fma(-rho, T.h[i], fma(-al, T.g[i], y[i])) : rho;
+          nv[i] = relax(cen[i], omega, xv);
+        }
+        GS_PROF(7, nv[NC - 1] + nv[0]);
+        // ---- hand the new row on -----------------------------------------
+        if (last) {
+          const int hs = j % DHL;
+          if (j >= DHL) gs_mbar_wait(&emptyL[hs], ((j / DHL) - 1) & 1);
+          double* h = HL + hs * SLOT;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) h[i * IS + lane] = nv[i];
+          __syncwarp();
+          if (lane == 0) gs_mbar_arrive(&fullL[hs]);
+        } else {
+          const int hs = j % DH;
+          if (consumer && j >= DH) gs_mbar_wait(&emptyH[warp * DH + hs], ((j / DH) - 1) & 1);
+          double* h = Hr + hs * SLOT;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) h[i * IS + lane] = nv[i];
+          __syncwarp();
+          if (consumer && lane == 0) gs_mbar_arrive(&fullH[warp * DH + hs]);
+          double* dst = row0 + (long long)j * px;
+#pragma unroll
+          for (int i = 0; i < NC; ++i) __stcg(dst + i * 32 + lane, h[dpos[i]]);
+        }
+        GS_PROF(8, 0.0);
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+          ym[i] = nv[i];
+          cen[i] = nxt[i];
+        }
+      }
+      cp_wait<0>();
+      if (warp == 0 && k > 0) mbase += (uint32_t)ny;
+    }
+    __syncthreads();
+  }
+}
+
+template <int NC, int CH, int UN>
+static int gs_pipe_occ1() {
+  using C = GCfg<NC>;
+  cudaFuncSetAttribute(line_gs_pipe_kernel<NC, CH, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, line_gs_pipe_kernel<NC, CH, UN>, kGsThreads, C::SMEM);
+  return b;
+}
+template <int NC>
+static int gs_pipe_occupancy() {
+  return std::min(std::min(gs_pipe_occ1<NC, 0, 0>(), gs_pipe_occ1<NC, 0, 1>()),
+                  std::min(gs_pipe_occ1<NC, 1, 0>(), gs_pipe_occ1<NC, 1, 1>()));
+}
+
+template <int NC>
+static cudaError_t gs_pipe_launch(int chaotic, int unit, int grid, const PatchDev* patches,
+                                  const unsigned char* active, const StencilDev& st, double omega, int* flags,
+                                  int* ticket, const int2* units, int nunits, const double* lane_tab,
+                                  const GsUniform& T, cudaStream_t s) {
+  using C = GCfg<NC>;
+#define PSM_GSP(CH, UN)                                                                                     \
+  line_gs_pipe_kernel<NC, CH, UN><<<grid, kGsThreads, C::SMEM, s>>>(patches, active, st, omega, flags, ticket, \
+                                                                    units, nunits, lane_tab, T)
+  if (chaotic) {
+    if (unit) PSM_GSP(1, 1); else PSM_GSP(1, 0);
+  } else {
+    if (unit) PSM_GSP(0, 1); else PSM_GSP(0, 0);
+  }
+#undef PSM_GSP
+  return cudaGetLastError();
+}
+
+}  // namespace psm
+
+using namespace psm;
+
+int psm_set_error(int code, const char* msg);
+
+// One group of patches sharing nx (= 32*NC): units, tables, launch geometry.
+struct GsPipeGroup {
+  int nc = 0;
+  int2* d_units = nullptr;
+  int nunits = 0;
+  double* d_tab = nullptr;  // [kGsTab][32]
+  GsUniform T{};
+  int grid = 0;
+  int ticket = 0;  // index of this group's ticket in the plan's flag array
+};
+
+struct GsPipeState {
+  std::vector<GsPipeGroup> groups;
+};
+
+#ifdef PSM_GS_PROFILE
+extern "C" int psm_debug_gs_profile(long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_gs_prof, sizeof(long long) * 16);
+  if (reset) {
+    long long z[16] = {0};
+    cudaMemcpyToSymbol(g_gs_prof, z, sizeof z);
+  }
+  return 0;
+}
+#endif
+
+bool gs_pipe_supported(int nx) { return nx == 32 || nx == 64 || nx == 128 || nx == 256; }
+
+// Host tables (long double) for the chunked line solve of order nx = 32*nc
+// with sub-diagonal lo, diagonal d and super-diagonal up.
+static int gs_pipe_tables(int nc, long double lo, long double d, long double up, GsUniform& T, double* lane_tab) {
+  const int m = nc - 1;
+  memset(&T, 0, sizeof T);
+  long double invm[8] = {0}, cp[8] = {0}, g[8] = {0}, h[8] = {0};
+  // Thomas factors of tridiag(lo, d, up) of order m
+  long double prev_cp = 0;
+  for (int i = 0; i < m; ++i) {
+    const long double mi = d - (i > 0 ? lo * prev_cp : 0.0L);
+    if (fabsl(mi) < 1e-14L * fabsl(d)) return psm_set_error(PSM_ESINGULAR, "line block pivot below 1e-14*|A|");
+    invm[i] = 1.0L / mi;
+    cp[i] = up * invm[i];
+    prev_cp = cp[i];
+  }
+  auto solve = [&](const long double* rhs, long double* x) {
+    long double y[8];
+    for (int i = 0; i < m; ++i) y[i] = (rhs[i] - (i > 0 ? lo * y[i - 1] : 0.0L)) * invm[i];
+    for (int i = m - 1; i >= 0; --i) x[i] = y[i] - (i < m - 1 ? cp[i] * x[i + 1] : 0.0L);
+  };
+  if (m > 0) {
+    long double e[8] = {0};
+    e[0] = lo;
+    solve(e, g);
+    e[0] = 0;
+    e[m - 1] = up;
+    solve(e, h);
+  }
+  for (int i = 0; i < m; ++i) {
+    T.invm[i] = (double)invm[i];
+    T.loinv[i] = (double)(lo * invm[i]);
+    T.cp[i] = (double)cp[i];
+    T.g[i] = (double)g[i];
+    T.h[i] = (double)h[i];
+  }
+  // interface system  A_L a_{L-1} + B_L a_L + C_L a_{L+1} = rhs_L
+  long double A[32], B[32], Cc[32];
+  for (int L = 0; L < 32; ++L) {
+    if (m == 0) {
+      A[L] = L > 0 ? lo : 0.0L;
+      B[L] = d;
+      Cc[L] = L < 31 ? up : 0.0L;
+    } else {
+      A[L] = L > 0 ? -lo * g[m - 1] : 0.0L;
+      B[L] = d - lo * h[m - 1] - (L < 31 ? up * g[0] : 0.0L);
+      Cc[L] = L < 31 ? -up * h[0] : 0.0L;
+    }
+    if (fabsl(B[L]) < 1e-14L * fabsl(d)) return psm_set_error(PSM_ESINGULAR, "line interface pivot below 1e-14*|A|");
+  }
+  long double al[32], ga[32];
+  for (int L = 0; L < 32; ++L) {
+    lane_tab[0 * 32 + L] = (double)(1.0L / B[L]);
+    lane_tab[1 * 32 + L] = m > 0 ? (double)(lo / B[L]) : 0.0;
+    lane_tab[2 * 32 + L] = (m > 0 && L < 31) ? (double)(up / B[L]) : 0.0;
+    al[L] = A[L] / B[L];
+    ga[L] = Cc[L] / B[L];
+  }
+  for (int t = 0; t < 5; ++t) {
+    const int dd = 1 << t;
+    long double na[32], ng[32];
+    for (int L = 0; L < 32; ++L) {
+      const long double gm = L - dd >= 0 ? ga[L - dd] : 0.0L, am = L - dd >= 0 ? al[L - dd] : 0.0L;
+      const long double ap = L + dd < 32 ? al[L + dd] : 0.0L, gp = L + dd < 32 ? ga[L + dd] : 0.0L;
+      const long double den = 1.0L - al[L] * gm - ga[L] * ap;
+      if (fabsl(den) < 1e-14L) return psm_set_error(PSM_ESINGULAR, "line PCR pivot below 1e-14");
+      lane_tab[(3 + 3 * t) * 32 + L] = (double)(1.0L / den);
+      lane_tab[(4 + 3 * t) * 32 + L] = (double)(al[L] / den);
+      lane_tab[(5 + 3 * t) * 32 + L] = (double)(ga[L] / den);
+      na[L] = -al[L] * am / den;
+      ng[L] = -ga[L] * gp / den;
+    }
+    memcpy(al, na, sizeof al);
+    memcpy(ga, ng, sizeof ga);
+    // couplings left after step t (normalised: unit diagonal); once they are
+    // below 1e-20 the remaining steps change a_L by < 1e-20 max|a|
+    long double cmax = 0;
+    for (int L = 0; L < 32; ++L) cmax = fmaxl(cmax, fmaxl(fabsl(al[L]), fabsl(ga[L])));
+    if (T.npcr == 0 && cmax < 1e-20L) T.npcr = t + 1;
+  }
+  if (T.npcr == 0) T.npcr = 5;
+  return PSM_OK;
+}
+
+// Builds the groups of the plan (all patches must have a supported nx);
+// flags: per global plane progress words, then one ticket per group.
+int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets) {
+  if (P->gspipe) {
+    *n_tickets = (int)P->gspipe->groups.size();
+    return PSM_OK;
+  }
+  GsPipeState* S = new GsPipeState();
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int nc : {1, 2, 4, 8}) {
+    // units (patch, k0) plane-group-major: every patch's first group comes
+    // before any second group, so independent patches fill the machine while
+    // each patch's CTA chain (group k0 waits on group k0-W) stays in order
+    std::vector<int> uv;
+    int maxnz = 0;
+    for (int p = 0; p < P->npatch; ++p) maxnz = std::max(maxnz, P->hp[p].nz);
+    for (int k0 = 0; k0 < maxnz; k0 += kGsW)
+      for (int p = 0; p < P->npatch; ++p) {
+        if (P->hp[p].nx != 32 * nc || k0 >= P->hp[p].nz) continue;
+        uv.push_back(p);
+        uv.push_back(k0);
+      }
+    if (uv.empty()) continue;
+    GsPipeGroup G;
+    G.nc = nc;
+    G.nunits = (int)(uv.size() / 2);
+    double tab[kGsTab * 32];
+    int rc = gs_pipe_tables(nc, (long double)P->st.xm, (long double)P->st.c, (long double)P->st.xp, G.T, tab);
+    if (rc) {
+      delete S;
+      return rc;
+    }
+    if (cudaMalloc(&G.d_units, uv.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&G.d_tab, sizeof tab) != cudaSuccess) {
+      delete S;
+      return psm_set_error(PSM_ENOMEM, "cudaMalloc for line GS units");
+    }
+    cudaMemcpy(G.d_units, uv.data(), uv.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(G.d_tab, tab, sizeof tab, cudaMemcpyHostToDevice);
+    int occ = 1;
+    switch (nc) {
+      case 1: occ = gs_pipe_occupancy<1>(); break;
+      case 2: occ = gs_pipe_occupancy<2>(); break;
+      case 4: occ = gs_pipe_occupancy<4>(); break;
+      default: occ = gs_pipe_occupancy<8>(); break;
+    }
+    if (occ < 1) {
+      delete S;
+      return psm_set_error(PSM_ECUDA, "line GS pipeline kernel does not fit on an SM");
+    }
+    G.grid = std::min(G.nunits, occ * sms);
+    G.ticket = (int)S->groups.size();
+    S->groups.push_back(G);
+  }
+  P->gspipe = S;
+  *n_tickets = (int)S->groups.size();
+  return PSM_OK;
+}
+
+void psm_gs_pipe_free(psm_plan* P) {
+  if (!P->gspipe) return;
+  for (auto& G : P->gspipe->groups) {
+    cudaFree(G.d_units);
+    cudaFree(G.d_tab);
+  }
+  delete P->gspipe;
+  P->gspipe = nullptr;
+}
+
+// flags: per-plane progress words (nplanes), tickets: one per group; both
+// zeroed by the caller on the stream before the launch.
+int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int chaotic, int* flags, int* tickets,
+                      cudaStream_t s) {
+  const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
+                    P->st.zm == -1.0 && P->st.zp == -1.0;
+  for (const GsPipeGroup& G : P->gspipe->groups) {
+    cudaError_t e;
+    int* tk = tickets + G.ticket;
+    switch (G.nc) {
+      case 1: e = gs_pipe_launch<1>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
+      case 2: e = gs_pipe_launch<2>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
+      case 4: e = gs_pipe_launch<4>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
+      default: e = gs_pipe_launch<8>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
+    }
+    if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
+    P->launches += 1;
+  }
+  return PSM_OK;
+}

@@ -1,0 +1,118 @@
+"""Per-configuration device timing of every BASELINE.json config on one GPU.
+
+One "step" is what the reference's smoother step does (smoother.py:138-169):
+the sweep plus the ghost refresh, without history.  Timed with CUDA events on
+the current stream over K steps after W warm-up steps; prints one JSON line
+per (config, scheme) with updates/s, GB/s at the 24 B/update algorithmic
+traffic, and for plane blocks the algorithmic fp64 TFLOP/s.
+
+    python tools/bench_configs.py [--only C3] [--steps K] [--warmup W]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1208_1975_b200 as ps  # noqa: E402
+from paper_1208_1975_b200.smoother import _Plan, _run  # noqa: E402
+from paper_1208_1975_b200.workloads import build_lattice  # noqa: E402
+
+
+def _fill(level, seed=0):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    for p in level.patches:
+        p.interior.copy_(torch.rand(p.interior.shape, dtype=torch.float64, device="cuda", generator=g))
+        p.f.copy_(torch.randn(p.f.shape, dtype=torch.float64, device="cuda", generator=g))
+
+
+def plane_flops(nx):
+    # two DST transforms (2*nx each) + modal Thomas (5) + residual (8) + relax (2)
+    return 4 * nx + 15
+
+
+def time_steps(level, cfg, steps, warmup):
+    plan = _Plan(level, cfg, ps.InverseCache())
+    ps.smoother._run(level, cfg, plan, warmup, False, None)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    _run(level, cfg, plan, steps, False, None)
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, plan
+
+
+def time_smooth(level, cfg):
+    """One full smooth() call (history included), device-timed."""
+    ps.smooth(level, cfg, ps.InverseCache())  # warm
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    ps.smooth(level, cfg, ps.InverseCache())
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+CONFIGS = {
+    "C1": dict(desc="64^3 single patch, line block Jacobi, 10 sweeps (smooth() incl. history)",
+               build=lambda: ps.build_level([(64, 64, 64)]), runs=[("block_jacobi", "line", None)], smooth_steps=10),
+    "C2": dict(desc="256^3 single patch, line GS: chaotic vs colour(wavefront)-ordered",
+               build=lambda: ps.build_level([(256, 256, 256)]),
+               runs=[("chaotic_block_gs", "line", "chaotic"), ("chaotic_block_gs", "line", "wavefront")]),
+    "C3": dict(desc="512^3 single patch, plane block Jacobi, exact plane inverse",
+               build=lambda: ps.build_level([(512, 512, 512)]), runs=[("block_jacobi", "plane", None)]),
+    "C4": dict(desc="AMR-style 4x4x4 lattice of 128^3 patches (288 interface copies), line/plane GS",
+               build=lambda: build_lattice((4, 4, 4), (128, 128, 128)),
+               runs=[("chaotic_block_gs", "line", "wavefront"), ("chaotic_block_gs", "line", "chaotic"),
+                     ("chaotic_block_gs", "plane", "wavefront"), ("block_jacobi", "line", None)]),
+    "C5": dict(desc="1024^3 uniform grid, line Jacobi, 1 GPU",
+               build=lambda: ps.build_level([(1024, 1024, 1024)]), runs=[("block_jacobi", "line", None)]),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default=None)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    a = ap.parse_args()
+    names = a.only.split(",") if a.only else list(CONFIGS)
+    for name in names:
+        C = CONFIGS[name]
+        level = C["build"]()
+        _fill(level)
+        cells = level.interior_cells
+        p0 = level.patches[0].dims
+        for scheme, kind, mode in C["runs"]:
+            bd = (p0.nx, 1, 1) if kind == "line" else (p0.nx, p0.ny, 1)
+            strat = ps.ExecutionStrategy.device(gs_mode=mode or "wavefront")
+            cfg = ps.SmootherConfig(scheme=scheme, block_dims=bd, strategy=strat)
+            ms, plan = time_steps(level, cfg, a.steps, a.warmup)
+            rec = {"config": name, "desc": C["desc"], "scheme": scheme, "block": kind, "gs_mode": mode,
+                   "cells": cells, "ms_per_step": round(ms, 4), "Gupdates_per_s": round(cells / ms / 1e6, 2),
+                   "GBps_at_24B": round(24 * cells / ms / 1e6, 1)}
+            if kind == "plane":
+                rec["TFLOPs_alg"] = round(plane_flops(p0.nx) * cells / ms / 1e9, 2)
+            if C.get("smooth_steps"):
+                cfg2 = ps.SmootherConfig(scheme=scheme, block_dims=bd, strategy=strat, steps=C["smooth_steps"])
+                tms = time_smooth(level, cfg2)
+                rec["smooth_call_ms"] = round(tms, 4)
+                rec["smooth_Gupdates_per_s"] = round(cells * C["smooth_steps"] / tms / 1e6, 2)
+            print(json.dumps(rec), flush=True)
+            del plan
+        del level
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
