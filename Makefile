@@ -10,7 +10,7 @@ HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/psmooth.h
 all: $(PKG)/libpsmooth.so oracle
 
 $(PKG)/libpsmooth.so: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcublas 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -Xlinker --no-undefined -o $@ $(SRCS) -lcublas -lcudart 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
 oracle:
 	$(MAKE) -C oracle

@@ -122,6 +122,16 @@ int psm_jacobi_sweep_planes(psm_plan* plan, const unsigned char* active, double 
 int psm_halo_unpack(psm_plan* plan, const unsigned char* active, int patch, int side, const double* plane_dev,
                     void* stream);
 
+/* Plane-block solver selection, process-wide: PSM_PLANE_AUTO (default) uses
+ * the banded factorised solve (block Thomas along y, Schur complements as
+ * short convolutions along x) wherever its truncation bound holds, else the
+ * DST-I form; PSM_PLANE_DST forces the DST-I form (cuBLAS DGEMM transforms).
+ * Both are exact block inverses to rounding (blocklinalg.py:116-163 replaced).
+ * mode < 0 only queries.  Returns the previous mode. */
+#define PSM_PLANE_AUTO 0
+#define PSM_PLANE_DST 1
+int psm_plane_solver(int mode);
+
 /* Number of kernels this plan has launched so far (benchmark evidence). */
 long long psm_plan_launches(const psm_plan* plan);
 

@@ -50,7 +50,10 @@ EXPORTS = (
     "psm_jacobi_sweep_planes",
     "psm_halo_unpack",
     "psm_plan_launches",
+    "psm_plane_solver",
 )
+PLANE_AUTO = 0
+PLANE_DST = 1
 
 
 class Stencil(ctypes.Structure):
@@ -124,6 +127,7 @@ def load():
             "psm_jacobi_sweep_planes": (i, [vp, ub, d, i, i, i, i, vp]),
             "psm_halo_unpack": (i, [vp, ub, i, i, vp, vp]),
             "psm_plan_launches": (ll, [vp]),
+            "psm_plane_solver": (i, [i]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -24,9 +24,21 @@ from . import _lib
 from .grid import _int3, default_device
 from .stencil import Stencil7
 
-__all__ = ["SingularMatrixError", "BlockFactors", "InverseCache", "block_kind"]
+__all__ = ["SingularMatrixError", "BlockFactors", "InverseCache", "block_kind", "plane_solver"]
 
 _MAX_DENSE = 8192
+
+
+def plane_solver(mode=None):
+    """Select the device form of the exact plane-block inverse, process-wide:
+    'auto' (default: the banded factorised block-Thomas solve wherever its
+    2e-18 truncation bound holds, else DST-I) or 'dst' (DST-I transforms as
+    cuBLAS DGEMMs).  Returns the previous mode; ``None`` only queries."""
+    modes = {"auto": _lib.PLANE_AUTO, "dst": _lib.PLANE_DST}
+    if mode is not None and mode not in modes:
+        raise ValueError(f"plane solver must be 'auto' or 'dst', got {mode!r}")
+    prev = _lib.load().psm_plane_solver(modes[mode] if mode is not None else -1)
+    return "dst" if prev == _lib.PLANE_DST else "auto"
 
 
 class SingularMatrixError(ValueError):

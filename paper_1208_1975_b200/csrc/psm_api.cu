@@ -25,7 +25,7 @@ bool line_nx_specialised(int nx);
 int zmarch_rows(int nx);
 cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
                                const StencilDev& st, double omega, double* partials, const void* units, int nunits,
-                               int grid, const LineFac& L, cudaStream_t stream);
+                               int grid, const LineFac& L, cudaStream_t stream, double* rglob = nullptr);
 int line_nx_occupancy(int nx);
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
@@ -78,6 +78,7 @@ int psm_plane_plan_setup(psm_plan* plan);  // psm_plane.cu
 int psm_plane_plan_free(psm_plan* plan);
 int psm_plane_jacobi(psm_plan* P, const unsigned char* d_active, double omega, double* partials, cudaStream_t s);
 int psm_plane_gs(psm_plan* P, const unsigned char* d_active, double omega, cudaStream_t s);
+extern int psm_plane_band_mode;  // psm_plane.cu
 // pipelined line GS (psm_line_gs_pipe.cu)
 bool gs_pipe_supported(int nx);
 int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets);
@@ -577,6 +578,43 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
   return PSM_OK;
 }
 
+// Residual r = f - A u of every cell into rbuf (cell-major, per patch at
+// cell0) plus the history partials, for the plane path: the z-marching TMA
+// kernel in residual-only mode where nx is specialised, else the tile kernel.
+int psm_plane_residual(psm_plan* P, const unsigned char* da, double* partials, double* rbuf, cudaStream_t s) {
+  const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
+                    P->st.zm == -1.0 && P->st.zp == -1.0;
+  int p = 0;
+  while (p < P->npatch) {
+    const int nx = P->hp[p].nx;
+    int q = p + 1;
+    while (q < P->npatch && P->hp[q].nx == nx) ++q;
+    if (P->tiled && line_nx_specialised(nx) && P->hp[p].R == zmarch_rows(nx)) {
+      void* units;
+      int nu;
+      int rc = zmarch_units(P, p, q, 0, -1, &units, &nu);
+      if (rc) return rc;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      LineFac dummy;
+      memset(&dummy, 0, sizeof dummy);
+      CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, 0.0, partials, units, nu, sms, dummy, s,
+                                  rbuf));
+      P->launches += 1;
+    } else {
+      for (int r = p; r < q; ++r) {
+        const PatchDev& h = P->hp[r];
+        CUDA_TRY(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, rbuf, h.tile0, h.tiles,
+                                   P->threads, 0, s));
+        P->launches += 1;
+      }
+    }
+    p = q;
+  }
+  return PSM_OK;
+}
+
 int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int slot, void* stream) {
   if (!P) return fail(PSM_EINVAL, "null plan");
   if (!(omega > 0.0 && omega <= 1.0)) return fail(PSM_EINVAL, "omega must lie in (0, 1], got %g", omega);
@@ -623,6 +661,13 @@ int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int sid
 }
 
 long long psm_plan_launches(const psm_plan* P) { return P ? P->launches : -1; }
+
+int psm_plane_solver(int mode) {
+  const int prev = psm_plane_band_mode == 0 ? PSM_PLANE_DST : PSM_PLANE_AUTO;
+  if (mode == PSM_PLANE_DST) psm_plane_band_mode = 0;
+  else if (mode == PSM_PLANE_AUTO) psm_plane_band_mode = -1;
+  return prev;
+}
 
 
 // Work units (patch, plane) in dependency order and the progress flags of

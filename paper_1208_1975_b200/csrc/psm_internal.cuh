@@ -45,6 +45,9 @@ struct PlaneFac {
   const double* Q;     // nx*nx orthonormal DST-I basis, symmetric
   const double* cp;    // [mode][ny] Thomas factors
   const double* invm;  // [mode][ny]
+  // banded factorised form (psm_plane_band.cu); bw == 0: not available
+  int bw, nj;          // convolution half-width, distinct leading Schur complements
+  const double* H;     // [nj+1][bw+1] symmetric kernels H_j(0..bw)
 };
 
 struct PatchDev {

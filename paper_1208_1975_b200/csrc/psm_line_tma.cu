@@ -28,6 +28,7 @@
 //                tile's r^2 partial.  B(k) overlaps A(k+1) of the A/C warps
 //                (double-buffered r / y buffers, named barriers).
 #include <stdint.h>
+#include <string.h>
 
 #include <type_traits>
 
@@ -92,7 +93,7 @@ struct ZCfg {
   static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * 8 + (2 * NU + 2 * NF) * 8 + 16;
 };
 
-constexpr int kBarR = 1, kBarY = 3;
+constexpr int kBarR = 1, kBarY = 3, kBarRes = 5;
 
 // Factor tables passed by value: they live in the kernel-parameter constant
 // bank, so the fully unrolled solver reads them as DFMA constant operands
@@ -121,7 +122,7 @@ __device__ __forceinline__ int cell_x(int q, int tid) {
 // row's y-1 and the last row's y+1 are read from the slab.  Three register
 // arrays rotate through the roles u(k-1), u(k), u(k+1) (the plane loop is
 // unrolled by three, so the queue never moves data).
-template <int NX, int UNIT>
+template <int NX, int UNIT, int RES>
 struct ZAC {
   using C = ZCfg<NX>;
   static constexpr int R = C::R, PX = C::PX, RS = C::RS, E = C::E, ACT = C::ACT;
@@ -134,6 +135,10 @@ struct ZAC {
   StencilDev st;
   double omega;
   double *uring, *fring, *rbuf, *wsum, *v;
+  double* rg = nullptr;        // RES: global residual of this patch (cell-major like f)
+  double* partials = nullptr;  // RES: per (plane, tile) r^2 partials
+  long long tslot0 = 0;        // RES: partial index of plane 0's tile
+  int tpp = 0, ny = 0;
   uint64_t *full_u, *empty_u, *full_f, *empty_f;
   long long pxy, vbase_old = 0;
   uint32_t nu = 0, nf = 0;
@@ -216,7 +221,10 @@ struct ZAC {
             res = residual7(st, fv, c[i], xl, xr, ym, yp, zm[i], zp[i]);
           }
           ssq = fma(res, res, ssq);
-          rb[row * RS + x + (x >> 5)] = res;
+          if (RES)
+            __stcs(rg + ((long long)k * ny + j0 + row) * NX + x, res);
+          else
+            rb[row * RS + x + (x >> 5)] = res;
         }
       }
     }
@@ -228,8 +236,20 @@ struct ZAC {
       mbar_arrive(&empty_u[s_cur]);
       mbar_arrive(&empty_f[t]);
     }
-    named_arrive(kBarR + b, NBAR);
-    if (k > k0) phaseC<FULL>(zm);  // u(k-1) is this plane's zm
+    if (RES) {
+      // residual-only (plane path): the A/C warps reduce the tile partial
+      // themselves, in the solver warps' fixed order
+      named_sync(kBarRes, ACT);
+      if (tid == 0 && partials) {
+        double tt = 0.0;
+#pragma unroll
+        for (int q = 0; q < C::AC_WARPS; ++q) tt += wsum[b * C::AC_WARPS + q];
+        partials[tslot0 + (long long)k * tpp + j0 / R] = tt;
+      }
+    } else {
+      named_arrive(kBarR + b, NBAR);
+      if (k > k0) phaseC<FULL>(zm);  // u(k-1) is this plane's zm
+    }
     vbase_old = (long long)(k + 1) * pxy + (long long)(j0 + 1) * PX + 1;
     s_cur = s_nxt;
     b ^= 1;
@@ -252,22 +272,25 @@ struct ZAC {
     int k = ka;
     for (;;) {
       step<FULL>(A0, A1, A2, k++);
-      if (k >= kb) { phaseC<FULL>(A1); break; }
+      if (k >= kb) { if (!RES) phaseC<FULL>(A1); break; }
       step<FULL>(A1, A2, A0, k++);
-      if (k >= kb) { phaseC<FULL>(A2); break; }
+      if (k >= kb) { if (!RES) phaseC<FULL>(A2); break; }
       step<FULL>(A2, A0, A1, k++);
-      if (k >= kb) { phaseC<FULL>(A0); break; }
+      if (k >= kb) { if (!RES) phaseC<FULL>(A0); break; }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_u[s_cur]);  // the unit's last slab (plane kb)
   }
 };
 
-template <int NX, int UNIT>
+// RES = 1: residual only (plane path): r = f - A u to rglob plus the tile
+// partials; no solver, no v.
+template <int NX, int UNIT, int RES>
 __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
     line_jacobi_zmarch_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
                               StencilDev st, double omega, double* __restrict__ partials,
-                              const ZUnit* __restrict__ units, int nunits, const __grid_constant__ ZTab T) {
+                              const ZUnit* __restrict__ units, int nunits, const __grid_constant__ ZTab T,
+                              double* __restrict__ rglob) {
   using C = ZCfg<NX>;
   constexpr int R = C::R, PX = C::PX, NSEG = C::NSEG, NSL = C::NSL, RS = C::RS, E = C::E, ACT = C::ACT;
   extern __shared__ __align__(128) double zsm[];
@@ -330,6 +353,7 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
 
   // ======================= solver warps ======================================
   if (warp >= C::AC_WARPS) {
+    if (RES) return;
     const int sl = tid - C::AC_WARPS * 32;  // 0..NSL-1
     const int r = sl / NSEG, s = sl % NSEG;
     const double lo = T.lo, up = T.up, up_h31 = T.up_h31, lo_g0 = T.lo_g0, d_full = T.d_full;
@@ -391,7 +415,7 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
   }
 
   // ======================= A/C warps =========================================
-  ZAC<NX, UNIT> ac;
+  ZAC<NX, UNIT, RES> ac;
   ac.tid = tid;
   ac.lane = lane;
   ac.warp = warp;
@@ -405,8 +429,9 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
   ac.empty_u = empty_u;
   ac.full_f = full_f;
   ac.empty_f = empty_f;
-  ac.tx = ZAC<NX, UNIT>::NX_GE ? tid : tid % NX;
-  ac.trow0 = ZAC<NX, UNIT>::NX_GE ? 0 : (tid / NX) * ZAC<NX, UNIT>::RPT;
+  ac.tx = ZAC<NX, UNIT, RES>::NX_GE ? tid : tid % NX;
+  ac.trow0 = ZAC<NX, UNIT, RES>::NX_GE ? 0 : (tid / NX) * ZAC<NX, UNIT, RES>::RPT;
+  ac.partials = partials;
   for (int w = blockIdx.x; w < nunits; w += gridDim.x) {
     const ZUnit U = units[w];
     const PatchDev& P = patches[U.patch];
@@ -415,6 +440,12 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
     ac.v = P.buf[active[U.patch] ^ 1];
     ac.j0 = U.j0;
     ac.k0 = U.k0;
+    if (RES) {
+      ac.rg = rglob + P.cell0;
+      ac.tslot0 = P.tile0;
+      ac.tpp = P.tpp;
+      ac.ny = P.ny;
+    }
     if (ac.rows == R)
       ac.template run_unit<true>(U.k0, U.k1);
     else
@@ -425,22 +456,30 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
 template <int NX>
 static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                            double omega, double* partials, const ZUnit* units, int nunits, int grid,
-                           const ZTab& T, cudaStream_t stream) {
+                           const ZTab& T, double* rglob, cudaStream_t stream) {
   using C = ZCfg<NX>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM_BYTES);
-    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM_BYTES);
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM_BYTES);
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM_BYTES);
     attr = true;
   }
-  if (unit)
-    line_jacobi_zmarch_kernel<NX, 1><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega,
-                                                                                  partials, units, nunits, T);
-  else
-    line_jacobi_zmarch_kernel<NX, 0><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega,
-                                                                                  partials, units, nunits, T);
+#define PSM_ZL(U_, R_)                                                                                         \
+  line_jacobi_zmarch_kernel<NX, U_, R_><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega, \
+                                                                                      partials, units, nunits, T, \
+                                                                                      rglob)
+  if (rglob) {
+    if (unit) PSM_ZL(1, 1); else PSM_ZL(0, 1);
+  } else {
+    if (unit) PSM_ZL(1, 0); else PSM_ZL(0, 0);
+  }
+#undef PSM_ZL
   return cudaGetLastError();
 }
 
@@ -448,11 +487,13 @@ int zmarch_rows(int nx) { return kMaxTileCells / nx; }
 
 cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
                                const StencilDev& st, double omega, double* partials, const void* units, int nunits,
-                               int grid, const LineFac& L, cudaStream_t stream) {
+                               int grid, const LineFac& L, cudaStream_t stream, double* rglob) {
   if (nunits <= 0) return cudaSuccess;
   if (grid > nunits) grid = nunits;
   const ZUnit* u = (const ZUnit*)units;
   ZTab T;
+  memset(&T, 0, sizeof T);
+  if (!rglob)
   for (int i = 0; i < kSeg; ++i) {
     T.invm[i] = L.invm[i];
     T.loinv[i] = L.lo * L.invm[i];
@@ -464,6 +505,7 @@ cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const 
     T.g16[i] = L.g16[i];
     T.h16[i] = L.h16[i];
   }
+  if (!rglob) {
   T.lo = L.lo;
   T.up = L.up;
   T.up_h31 = L.up_h31;
@@ -472,12 +514,13 @@ cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const 
   T.up_h16 = L.up_h16;
   T.lo_g16 = L.lo_g16;
   T.d16 = L.d16;
+  }
   switch (nx) {
-    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
-    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
-    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
-    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
-    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, T, stream);
+    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
+    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
+    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
+    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
+    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
     default: return cudaErrorInvalidValue;
   }
 }

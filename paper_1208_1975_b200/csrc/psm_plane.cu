@@ -25,6 +25,12 @@
 #include "psm_internal.cuh"
 
 namespace psm {
+void plane_band_tables(long double c, long double a, long double blo, long double bup, int nx, int ny, int* bw_out,
+                       int* nj_out, std::vector<double>& H);
+int band_k_for(int nx);
+cudaError_t launch_plane_band_jacobi(int K, int BW, const PatchDev* patches, const unsigned char* active,
+                                     double omega, const double* rbuf, double* zbuf, const int2* units,
+                                     int nunits, const double* hinf_host, cudaStream_t s);
 cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
                               const StencilDev& st, double omega, double* partials, double* rbuf, long long tile_base,
                               long long ntiles, int threads, size_t smem, cudaStream_t stream);
@@ -85,9 +91,10 @@ __global__ void plane_modal_thomas_kernel(const PlaneFac* __restrict__ F, double
 // physical x-face ghosts of v (fused, see psm_line.cu).
 __global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
                                    const unsigned char* __restrict__ active, double omega,
-                                   const double* __restrict__ xbuf, long long total) {
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
-       g += (long long)gridDim.x * blockDim.x) {
+                                   const double* __restrict__ xbuf, long long total, long long first) {
+  for (long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; g0 < total;
+       g0 += (long long)gridDim.x * blockDim.x) {
+    const long long g = g0 + first;  // cells [first, first + total); xbuf starts at cell `first`
     int lo = 0, hi = npatch - 1;
     while (lo < hi) {
       int mid = (lo + hi + 1) >> 1;
@@ -102,7 +109,7 @@ __global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npa
     const long long px = nx + 2, pxy = px * (ny + 2);
     const int act = active[lo];
     const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
-    const double nv = relax(P.buf[act][iu], omega, xbuf[g]);
+    const double nv = relax(P.buf[act][iu], omega, xbuf[g0]);
     double* v = P.buf[act ^ 1];
     v[iu] = nv;
     if (x == 0) v[iu - 1] = -nv;
@@ -151,7 +158,12 @@ struct PlaneRun {  // consecutive patches sharing one PlaneFac (same nx, ny)
   const PlaneFac* d_fac;
   const double* Q;
   int nx, ny;
+  int bw = 0;              // banded factorised solve available (psm_plane_band.cu)
+  int2* d_units = nullptr;  // (patch, plane) units of the run for the banded kernel
+  int nunits = 0;
+  std::vector<double> hinf;  // converged kernel H_nj (host copy, passed by value)
 };
+int psm_plane_band_mode = -1;  // -1: auto (banded where available), 0: DST only (tests/bench)
 
 struct PlaneState {
   cublasHandle_t handle = nullptr;
@@ -161,6 +173,7 @@ struct PlaneState {
   double* shat = nullptr;
   long long* d_stage_off = nullptr;
   long long stage_total = 0;
+
   std::vector<long long> stage_off;
   std::vector<PlaneRun> runs;
 };
@@ -168,6 +181,8 @@ struct PlaneState {
 
 // error plumbing shared with psm_api.cu
 int psm_set_error(int code, const char* msg);
+extern "C" int psm_plane_residual(psm_plan* P, const unsigned char* da, double* partials, double* rbuf,
+                                  cudaStream_t s);  // psm_api.cu
 
 #define PCUDA(expr)                                                                      \
   do {                                                                                   \
@@ -205,7 +220,10 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
       prev = yup / m;
     }
   }
-  const size_t bytes = sizeof(PlaneFac) + (nq + 2 * nt) * sizeof(double);
+  int bw = 0, nj = 0;
+  std::vector<double> band;
+  plane_band_tables(c, a, ylo, yup, nx, ny, &bw, &nj, band);
+  const size_t bytes = sizeof(PlaneFac) + (nq + 2 * nt + band.size()) * sizeof(double);
   if (cudaMalloc(&F->dev, bytes) != cudaSuccess) return psm_set_error(PSM_ENOMEM, "cudaMalloc for plane factors");
   double* tab = (double*)((char*)F->dev + sizeof(PlaneFac));
   PlaneFac& H = F->h_plane;
@@ -217,11 +235,16 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
   H.Q = tab;
   H.cp = tab + nq;
   H.invm = tab + nq + nt;
+  H.bw = bw;
+  H.nj = nj;
+  H.H = band.empty() ? nullptr : tab + nq + 2 * nt;
   F->d_plane = (PlaneFac*)F->dev;
   PCUDA(cudaMemcpy(F->dev, &H, sizeof H, cudaMemcpyHostToDevice));
   PCUDA(cudaMemcpy(tab, Q.data(), nq * sizeof(double), cudaMemcpyHostToDevice));
   PCUDA(cudaMemcpy(tab + nq, cp.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
   PCUDA(cudaMemcpy(tab + nq + nt, invm.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
+  if (!band.empty())
+    PCUDA(cudaMemcpy(tab + nq + 2 * nt, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice));
   return PSM_OK;
 }
 
@@ -289,6 +312,22 @@ int psm_plane_plan_setup(psm_plan* P) {
     r.Q = P->fac[p]->h_plane.Q;
     r.nx = P->hp[p].nx;
     r.ny = P->hp[p].ny;
+    r.bw = P->fac[p]->h_plane.bw;
+    if (r.bw > 0) {
+      const PlaneFac& hf = P->fac[p]->h_plane;
+      r.hinf.resize(hf.bw + 1);
+      PCUDA(cudaMemcpy(r.hinf.data(), hf.H + (size_t)hf.nj * (hf.bw + 1), (hf.bw + 1) * sizeof(double),
+                       cudaMemcpyDeviceToHost));
+      std::vector<int> uv;
+      for (int q2 = p; q2 < q; ++q2)
+        for (int k = 0; k < P->hp[q2].nz; ++k) {
+          uv.push_back(q2);
+          uv.push_back(k);
+        }
+      r.nunits = (int)(uv.size() / 2);
+      PCUDA(cudaMalloc(&r.d_units, uv.size() * sizeof(int)));
+      PCUDA(cudaMemcpy(r.d_units, uv.data(), uv.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
     S->runs.push_back(r);
     p = q;
   }
@@ -304,23 +343,36 @@ int psm_plane_plan_free(psm_plan* P) {
   cudaFree(S->sbuf);
   cudaFree(S->shat);
   cudaFree(S->d_stage_off);
+  for (auto& r : S->runs) cudaFree(r.d_units);
   delete S;
   P->plane = nullptr;
   return PSM_OK;
 }
 
-// Jacobi: residual of every cell (tile kernel, mode 2 stores r) -> DST ->
-// modal Thomas -> DST back -> relax into v.
+// Jacobi: residual of every cell (tile kernel, mode 2 stores r and the
+// history partials), then per run of patches sharing a factor either the
+// banded factorised solve (writes v directly) or DST -> modal Thomas -> DST
+// back -> relax into v.
 int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double* partials, cudaStream_t s) {
   PlaneState* S = P->plane;
-  PCUDA(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, S->rbuf, 0, P->ntiles, P->threads, 0,
-                          s));
-  P->launches += 2 + (long long)S->runs.size();  // residual, modal Thomas per run, relax
+  {
+    const int rc = psm_plane_residual(P, da, partials, S->rbuf, s);
+    if (rc) return rc;
+  }
   cublasSetStream(S->handle, s);
   for (const PlaneRun& r : S->runs) {
     const long long c0 = P->hp[r.p0].cell0;
-    long long planes = 0;
-    for (int p = r.p0; p < r.p1; ++p) planes += P->hp[p].nz;
+    long long planes = 0, cells = 0;
+    for (int p = r.p0; p < r.p1; ++p) {
+      planes += P->hp[p].nz;
+      cells += (long long)P->hp[p].nx * P->hp[p].ny * P->hp[p].nz;
+    }
+    if (r.bw > 0 && psm_plane_band_mode != 0) {
+      PCUDA(launch_plane_band_jacobi(band_k_for(r.nx), r.bw, P->d_patches, da, omega, S->rbuf, S->rhat, r.d_units,
+                                     r.nunits, r.hinf.data(), s));
+      P->launches += 1;
+      continue;
+    }
     const long long nvec = planes * r.ny;
     int rc = dst_gemm(S->handle, r.Q, r.nx, S->rbuf + c0, S->rhat + c0, nvec);
     if (rc) return rc;
@@ -328,11 +380,11 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
     PCUDA(cudaGetLastError());
     rc = dst_gemm(S->handle, r.Q, r.nx, S->rhat + c0, S->rbuf + c0, nvec);
     if (rc) return rc;
+    plane_relax_kernel<<<blocks_for(cells, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega, S->rbuf + c0,
+                                                              cells, c0);
+    PCUDA(cudaGetLastError());
+    P->launches += 4;
   }
-  long long cells = 0;
-  for (auto& h : P->hp) cells += (long long)h.nx * h.ny * h.nz;
-  plane_relax_kernel<<<blocks_for(cells, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega, S->rbuf, cells);
-  PCUDA(cudaGetLastError());
   return PSM_OK;
 }
 

@@ -70,7 +70,8 @@ CONFIGS = {
                build=lambda: ps.build_level([(256, 256, 256)]),
                runs=[("chaotic_block_gs", "line", "chaotic"), ("chaotic_block_gs", "line", "wavefront")]),
     "C3": dict(desc="512^3 single patch, plane block Jacobi, exact plane inverse",
-               build=lambda: ps.build_level([(512, 512, 512)]), runs=[("block_jacobi", "plane", None)]),
+               build=lambda: ps.build_level([(512, 512, 512)]),
+               runs=[("block_jacobi", "plane", None), ("block_jacobi", "plane", "dst")]),
     "C4": dict(desc="AMR-style 4x4x4 lattice of 128^3 patches (288 interface copies), line/plane GS",
                build=lambda: build_lattice((4, 4, 4), (128, 128, 128)),
                runs=[("chaotic_block_gs", "line", "wavefront"), ("chaotic_block_gs", "line", "chaotic"),
@@ -95,14 +96,22 @@ def main():
         p0 = level.patches[0].dims
         for scheme, kind, mode in C["runs"]:
             bd = (p0.nx, 1, 1) if kind == "line" else (p0.nx, p0.ny, 1)
-            strat = ps.ExecutionStrategy.device(gs_mode=mode or "wavefront")
+            solver = "dst" if mode == "dst" else "auto"
+            gs_mode = mode if mode in ("wavefront", "chaotic") else "wavefront"
+            strat = ps.ExecutionStrategy.device(gs_mode=gs_mode)
             cfg = ps.SmootherConfig(scheme=scheme, block_dims=bd, strategy=strat)
-            ms, plan = time_steps(level, cfg, a.steps, a.warmup)
+            prev = ps.plane_solver(solver)
+            try:
+                ms, plan = time_steps(level, cfg, a.steps, a.warmup)
+            finally:
+                ps.plane_solver(prev)
             rec = {"config": name, "desc": C["desc"], "scheme": scheme, "block": kind, "gs_mode": mode,
                    "cells": cells, "ms_per_step": round(ms, 4), "Gupdates_per_s": round(cells / ms / 1e6, 2),
                    "GBps_at_24B": round(24 * cells / ms / 1e6, 1)}
             if kind == "plane":
-                rec["TFLOPs_alg"] = round(plane_flops(p0.nx) * cells / ms / 1e9, 2)
+                rec["plane_solver"] = solver
+                if solver == "dst":
+                    rec["TFLOPs_alg"] = round(plane_flops(p0.nx) * cells / ms / 1e9, 2)
             if C.get("smooth_steps"):
                 cfg2 = ps.SmootherConfig(scheme=scheme, block_dims=bd, strategy=strat, steps=C["smooth_steps"])
                 tms = time_smooth(level, cfg2)
