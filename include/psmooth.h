@@ -132,6 +132,17 @@ int psm_halo_unpack(psm_plan* plan, const unsigned char* active, int patch, int 
 #define PSM_PLANE_DST 1
 int psm_plane_solver(int mode);
 
+/* A whole smooth() step sequence (smoother.py:197-214) as one stream-ordered
+ * call: scheme 0 = block Jacobi (steps x: sweep, swap, refresh with x faces
+ * skipped), 1 = block GS with mode gs_mode (steps x: sweep, refresh).  With
+ * history != 0 the leading refresh and the history[0..steps] residual
+ * partials are included (slots 0..steps must be reserved).  The first call
+ * with a given (scheme, omega, steps, gs_mode, history, active) runs eagerly;
+ * later ones replay a CUDA graph captured on the second call.  `active` is
+ * updated in place to the flags after the steps. */
+int psm_smooth_steps(psm_plan* plan, unsigned char* active, int scheme, double omega, int steps, int gs_mode,
+                     int history, void* stream);
+
 /* Number of kernels this plan has launched so far (benchmark evidence). */
 long long psm_plan_launches(const psm_plan* plan);
 

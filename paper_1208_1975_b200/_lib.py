@@ -51,6 +51,7 @@ EXPORTS = (
     "psm_halo_unpack",
     "psm_plan_launches",
     "psm_plane_solver",
+    "psm_smooth_steps",
 )
 PLANE_AUTO = 0
 PLANE_DST = 1
@@ -128,6 +129,7 @@ def load():
             "psm_halo_unpack": (i, [vp, ub, i, i, vp, vp]),
             "psm_plan_launches": (ll, [vp]),
             "psm_plane_solver": (i, [i]),
+            "psm_smooth_steps": (i, [vp, ub, i, d, i, i, i, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

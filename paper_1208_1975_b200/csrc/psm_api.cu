@@ -402,6 +402,9 @@ int psm_plan_destroy(psm_plan* P) {
   for (auto& kv : P->unit_cache) cudaFree(kv.second.first);
   for (auto& kv : P->active_cache) cudaFree(kv.second);
   if (P->kind == PSM_BLOCK_PLANE) psm_plane_plan_free(P);
+  for (auto& kv : P->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
   delete P;
   return PSM_OK;
 }
@@ -426,6 +429,10 @@ int psm_plan_reserve_history(psm_plan* P, int slots) {
   cudaFree(P->d_partials);
   cudaFree(P->d_plane_sums);
   cudaFree(P->d_sums);
+  // captured graphs hold the old history pointers: drop them (re-captured)
+  for (auto& kv : P->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  P->graphs.clear();
   P->d_partials = np;
   P->d_plane_sums = ns;
   P->d_sums = nt;
@@ -661,6 +668,95 @@ int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int sid
 }
 
 long long psm_plan_launches(const psm_plan* P) { return P ? P->launches : -1; }
+// The launch sequence of smooth() (smoother.py:197-214) for `steps` steps:
+// Jacobi: [refresh] then steps x (sweep into the inactive buffers with the
+// history slot, all patches swap, refresh with the x faces skipped) [, final
+// residual]; GS: [refresh, residual] then steps x (sweep, refresh [,
+// residual]).  `act` is updated to the active flags after the steps.
+static int smooth_sequence(psm_plan* P, std::vector<unsigned char>& act, int scheme, double omega, int steps,
+                           int gs_mode, int history, void* stream) {
+  int rc;
+  if (history) {
+    rc = psm_refresh_ghosts(P, act.data(), PSM_GHOST_ALL, stream);
+    if (rc) return rc;
+  }
+  if (scheme == 0) {
+    for (int s = 0; s < steps; ++s) {
+      rc = psm_jacobi_sweep(P, act.data(), omega, history ? s : -1, stream);
+      if (rc) return rc;
+      for (auto& a : act) a ^= 1;
+      rc = psm_refresh_ghosts(P, act.data(), PSM_GHOST_ALL | PSM_GHOST_SKIP_X, stream);
+      if (rc) return rc;
+    }
+    if (history) return psm_residual(P, act.data(), steps, stream);
+    return PSM_OK;
+  }
+  if (history) {
+    rc = psm_residual(P, act.data(), 0, stream);
+    if (rc) return rc;
+  }
+  for (int s = 0; s < steps; ++s) {
+    rc = psm_gs_sweep(P, act.data(), omega, gs_mode, stream);
+    if (rc) return rc;
+    rc = psm_refresh_ghosts(P, act.data(), PSM_GHOST_ALL, stream);
+    if (rc) return rc;
+    if (history) {
+      rc = psm_residual(P, act.data(), s + 1, stream);
+      if (rc) return rc;
+    }
+  }
+  return PSM_OK;
+}
+
+int psm_smooth_steps(psm_plan* P, unsigned char* active, int scheme, double omega, int steps, int gs_mode,
+                     int history, void* stream) {
+  if (!P || !active) return fail(PSM_EINVAL, "null argument");
+  if (scheme != 0 && scheme != 1) return fail(PSM_EINVAL, "scheme must be 0 (Jacobi) or 1 (GS), got %d", scheme);
+  if (steps < 1) return fail(PSM_EINVAL, "steps must be positive, got %d", steps);
+  if (history && steps + 1 > P->cap_slots) return fail(PSM_EINVAL, "history needs %d reserved slots", steps + 1);
+  std::vector<unsigned char> act(active, active + P->npatch);
+  for (unsigned char a : act)
+    if (a > 1) return fail(PSM_EINVAL, "active flags must be 0 or 1");
+  char kb[96];
+  snprintf(kb, sizeof kb, "%d:%a:%d:%d:%d:", scheme, omega, steps, gs_mode, history);
+  auto& G = P->graphs[std::string(kb) + std::string((const char*)active, P->npatch)];
+  if (G.exec == nullptr && G.seen == 0) {
+    // first call with this key: eager, which also performs every lazy
+    // allocation (active vectors, work units, factor tables, workspaces)
+    G.seen = 1;
+    const int rc = smooth_sequence(P, act, scheme, omega, steps, gs_mode, history, stream);
+    if (rc) return rc;
+  } else {
+    if (G.exec == nullptr) {  // second call: capture once, replay from now on
+      if (!P->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking));
+      const long long before = P->launches;
+      CUDA_TRY(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const int rc = smooth_sequence(P, act, scheme, omega, steps, gs_mode, history, P->cap_stream);
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(P->cap_stream, &graph);
+      if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (ce != cudaSuccess) return fail(PSM_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) {
+        G.exec = nullptr;
+        return fail(PSM_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+      }
+      G.kernels = P->launches - before;
+      P->launches = before;
+    }
+    CUDA_TRY(cudaGraphLaunch(G.exec, (cudaStream_t)stream));
+    P->launches += G.kernels;
+  }
+  // the active flags after the steps (Jacobi swaps every patch once per step)
+  if (scheme == 0 && (steps & 1))
+    for (int i = 0; i < P->npatch; ++i) active[i] ^= 1;
+  return PSM_OK;
+}
+
 
 int psm_plane_solver(int mode) {
   const int prev = psm_plane_band_mode == 0 ? PSM_PLANE_DST : PSM_PLANE_AUTO;

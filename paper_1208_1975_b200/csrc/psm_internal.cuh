@@ -173,5 +173,13 @@ struct psm_plan {
   int gs_ntickets = 0;
   // plane path
   PlaneState* plane = nullptr;
+  // CUDA graphs of whole smooth() step sequences (psm_smooth_steps)
+  cudaStream_t cap_stream = nullptr;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    long long kernels = 0;  // launches recorded at capture, added per replay
+    int seen = 0;           // eager runs so far (capture on the second call)
+  };
+  std::map<std::string, GraphEntry> graphs;
 };
 

@@ -66,6 +66,7 @@ __global__ void plane_stage_residual_kernel(const PatchDev* __restrict__ patches
 // PlaneFac.  Layout: plane-major, then y, then mode (x-mode fastest), so
 // threads of a warp take consecutive modes (coalesced).  In place.
 __global__ void plane_modal_thomas_kernel(const PlaneFac* __restrict__ F, double* __restrict__ buf, long long nplanes) {
+  constexpr int B = 16;  // rows per batch: the loads of a batch are issued together (latency once per B rows)
   const int nx = F->nx, ny = F->ny;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= nplanes * nx) return;
@@ -76,12 +77,40 @@ __global__ void plane_modal_thomas_kernel(const PlaneFac* __restrict__ F, double
   const double* invm = F->invm + i;
   const double lo = F->fy_lo;
   double prev = 0.0;
-  for (int j = 0; j < ny; ++j) {
+  int j = 0;
+  for (; j + B <= ny; j += B) {
+    double v[B], m[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      v[q] = b[(long long)(j + q) * nx];
+      m[q] = __ldg(invm + (long long)(j + q) * nx);
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      prev = fma(-lo, prev, v[q]) * m[q];
+      b[(long long)(j + q) * nx] = prev;
+    }
+  }
+  for (; j < ny; ++j) {
     prev = fma(-lo, prev, b[(long long)j * nx]) * invm[(long long)j * nx];
     b[(long long)j * nx] = prev;
   }
   double next = prev;
-  for (int j = ny - 2; j >= 0; --j) {
+  j = ny - 2;
+  for (; j - B + 1 >= 0; j -= B) {
+    double v[B], c[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      v[q] = b[(long long)(j - q) * nx];
+      c[q] = __ldg(cp + (long long)(j - q) * nx);
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      next = fma(-c[q], next, v[q]);
+      b[(long long)(j - q) * nx] = next;
+    }
+  }
+  for (; j >= 0; --j) {
     next = fma(-cp[(long long)j * nx], next, b[(long long)j * nx]);
     b[(long long)j * nx] = next;
   }
@@ -117,11 +146,14 @@ __global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npa
   }
 }
 
-// GS epilogue for stage k: u = u + omega * x in place on plane k.
-__global__ void plane_stage_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
-                                         const unsigned char* __restrict__ active, double omega, int k,
-                                         const long long* __restrict__ stage_off, const double* __restrict__ xbuf,
-                                         long long total) {
+// GS stage k epilogue fused with stage k+1's residual: u(k) += omega x in
+// place, then r(k+1) = f - A u at the same (x, y), which reads u(k) only at
+// this cell (its z-neighbour, just updated by this thread) and plane k+1's
+// old values; r(k+1) overwrites x in the stage buffer (same element).
+__global__ void plane_stage_relax_residual_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                                  const unsigned char* __restrict__ active, StencilDev st,
+                                                  double omega, int k, const long long* __restrict__ stage_off,
+                                                  double* __restrict__ sbuf, long long total) {
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
     int lo = 0, hi = npatch - 1;
@@ -130,7 +162,6 @@ __global__ void plane_stage_relax_kernel(const PatchDev* __restrict__ patches, i
       if (stage_off[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const PatchDev& P = patches[lo];
-    if (k >= P.nz) continue;
     const long long e = g - stage_off[lo];
     const int nx = P.nx, ny = P.ny;
     if (e >= (long long)nx * ny) continue;
@@ -138,7 +169,17 @@ __global__ void plane_stage_relax_kernel(const PatchDev* __restrict__ patches, i
     const long long px = nx + 2, pxy = px * (ny + 2);
     double* u = P.buf[active[lo]];
     const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
-    u[iu] = relax(u[iu], omega, xbuf[g]);
+    double un = 0.0;
+    if (k < P.nz) {
+      un = relax(u[iu], omega, sbuf[g]);
+      u[iu] = un;
+    }
+    if (k + 1 < P.nz) {
+      const long long iv = iu + pxy;  // (x, j, k+1)
+      const double zm = (k < P.nz) ? un : u[iv - pxy];
+      sbuf[g] = residual7(st, P.f[((long long)(k + 1) * ny + j) * nx + x], u[iv], u[iv - 1], u[iv + 1], u[iv - px],
+                          u[iv + px], zm, u[iv + pxy]);
+    }
   }
 }
 
@@ -165,8 +206,10 @@ struct PlaneRun {  // consecutive patches sharing one PlaneFac (same nx, ny)
 };
 int psm_plane_band_mode = -1;  // -1: auto (banded where available), 0: DST only (tests/bench)
 
+constexpr size_t kBlasWs = 32u << 20;
 struct PlaneState {
   cublasHandle_t handle = nullptr;
+  void* blas_ws = nullptr;
   double* rbuf = nullptr;   // sum of cells: residual, then x
   double* rhat = nullptr;   // sum of cells: modal coefficients
   double* sbuf = nullptr;   // GS stage buffers (sum over patches of nx*ny), x2
@@ -287,6 +330,9 @@ int psm_plane_plan_setup(psm_plan* P) {
   PlaneState* S = new PlaneState();
   P->plane = S;
   PBLAS(cublasCreate(&S->handle));
+  // explicit workspace: cuBLAS must not allocate while a CUDA graph captures
+  PCUDA(cudaMalloc(&S->blas_ws, kBlasWs));
+  PBLAS(cublasSetWorkspace(S->handle, S->blas_ws, kBlasWs));
   long long cells = 0;
   for (auto& h : P->hp) cells += (long long)h.nx * h.ny * h.nz;
   PCUDA(cudaMalloc(&S->rbuf, cells * sizeof(double)));
@@ -338,6 +384,7 @@ int psm_plane_plan_free(psm_plan* P) {
   PlaneState* S = P->plane;
   if (!S) return PSM_OK;
   if (S->handle) cublasDestroy(S->handle);
+  cudaFree(S->blas_ws);
   cudaFree(S->rbuf);
   cudaFree(S->rhat);
   cudaFree(S->sbuf);
@@ -395,11 +442,11 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
   cublasSetStream(S->handle, s);
   int maxnz = 0;
   for (auto& h : P->hp) maxnz = std::max(maxnz, h.nz);
+  plane_stage_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, P->st, 0,
+                                                                             S->d_stage_off, S->sbuf, S->stage_total);
+  PCUDA(cudaGetLastError());
+  P->launches += 1;
   for (int k = 0; k < maxnz; ++k) {
-    P->launches += 2;
-    plane_stage_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(
-        P->d_patches, P->npatch, da, P->st, k, S->d_stage_off, S->sbuf, S->stage_total);
-    PCUDA(cudaGetLastError());
     for (const PlaneRun& r : S->runs) {
       // patches of the run that still have plane k (nz may differ)
       int p0 = r.p0;
@@ -413,16 +460,18 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
         if (rc) return rc;
         plane_modal_thomas_kernel<<<(unsigned)((nplanes * r.nx + 127) / 128), 128, 0, s>>>(r.d_fac, S->shat + o,
                                                                                            nplanes);
-        P->launches += 1;
         PCUDA(cudaGetLastError());
         rc = dst_gemm(S->handle, r.Q, r.nx, S->shat + o, S->sbuf + o, nplanes * r.ny);
         if (rc) return rc;
+        P->launches += 3;
         p0 = p1;
       }
     }
-    plane_stage_relax_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega, k,
-                                                                            S->d_stage_off, S->sbuf, S->stage_total);
+    // relax stage k and form stage k+1's residual in one pass
+    plane_stage_relax_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(
+        P->d_patches, P->npatch, da, P->st, omega, k, S->d_stage_off, S->sbuf, S->stage_total);
     PCUDA(cudaGetLastError());
+    P->launches += 1;
   }
   return PSM_OK;
 }

@@ -160,7 +160,13 @@ def _swap_all(level):
 
 
 def _run(level, config, plan, steps, history, timers):
-    """Shared driver: returns the list of squared history entries (or None)."""
+    """Shared driver: returns the list of squared history entries (or None).
+
+    Without ``timers`` the whole step sequence is one ``psm_smooth_steps``
+    call, which replays a captured CUDA graph from the second call with the
+    same shape on; with ``timers`` (per-refresh CUDA events) it runs eagerly."""
+    if timers is None:
+        return _run_graph(level, config, plan, steps, history)
     dp = plan.dev
     gt = _GhostTimer(timers, plan.device)
     with torch.cuda.device(plan.device):
@@ -188,6 +194,23 @@ def _run(level, config, plan, steps, history, timers):
                     dp.residual(s + 1)
         sums = dp.sumsq(steps + 1) if history else None
     gt.commit()
+    return sums
+
+
+def _run_graph(level, config, plan, steps, history):
+    dp = plan.dev
+    jac = config.scheme == "block_jacobi"
+    with torch.cuda.device(plan.device):
+        if history:
+            dp.reserve(steps + 1)
+        act = dp._act()
+        _lib.check(_lib.load().psm_smooth_steps(dp.handle, act, 0 if jac else 1, float(config.omega), int(steps),
+                                                _gs_mode(config), 1 if history else 0, dp._stream()),
+                   "smooth_steps")
+        if jac:
+            for _ in range(steps):
+                _swap_all(level)
+        sums = dp.sumsq(steps + 1) if history else None
     return sums
 
 

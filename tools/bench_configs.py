@@ -50,17 +50,22 @@ def time_steps(level, cfg, steps, warmup):
     return e0.elapsed_time(e1) / steps, plan
 
 
-def time_smooth(level, cfg):
-    """One full smooth() call (history included), device-timed."""
-    ps.smooth(level, cfg, ps.InverseCache())  # warm
+def time_smooth(level, cfg, reps=20):
+    """Full smooth() calls (history included, one D2H each), device-timed,
+    with one warm InverseCache like the reference's run_bench (bench.py:211):
+    the first call runs eagerly, the second captures the CUDA graph."""
+    cache = ps.InverseCache()
+    for _ in range(3):
+        ps.smooth(level, cfg, cache)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    ps.smooth(level, cfg, ps.InverseCache())
+    for _ in range(reps):
+        ps.smooth(level, cfg, cache)
     e1.record(s)
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1)
+    return e0.elapsed_time(e1) / reps
 
 
 CONFIGS = {
@@ -86,6 +91,7 @@ def main():
     ap.add_argument("--only", default=None)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--runs", default=None, help="comma list of run indices within each config")
     a = ap.parse_args()
     names = a.only.split(",") if a.only else list(CONFIGS)
     for name in names:
@@ -94,7 +100,10 @@ def main():
         _fill(level)
         cells = level.interior_cells
         p0 = level.patches[0].dims
-        for scheme, kind, mode in C["runs"]:
+        sel = [int(x) for x in a.runs.split(",")] if a.runs else range(len(C["runs"]))
+        for ri, (scheme, kind, mode) in enumerate(C["runs"]):
+            if ri not in sel:
+                continue
             bd = (p0.nx, 1, 1) if kind == "line" else (p0.nx, p0.ny, 1)
             solver = "dst" if mode == "dst" else "auto"
             gs_mode = mode if mode in ("wavefront", "chaotic") else "wavefront"
