@@ -82,7 +82,13 @@ struct ZCfg {
   static constexpr int NSEG = NX / kSeg;
   static constexpr int NSL = R * NSEG;  // 64 segment lanes
   static constexpr int RS = NX + NSEG;  // padded r row
-  static constexpr int NU = 4, NF = 2;  // ring slots
+  // ring slots; deeper rings (4/3, 4/4, 5/3) measured no better on B200
+  // (tools/ztune.sh: within +-3% run to run at 512^3 and 1024^3)
+#ifdef PSM_ZNU
+  static constexpr int NU = PSM_ZNU, NF = PSM_ZNF;  // tuning builds
+#else
+  static constexpr int NU = 4, NF = 2;
+#endif
   static constexpr int US = (R + 2) * PX;  // doubles per u slot
   static constexpr int FS = R * NX;
   static constexpr int RB = R * RS;

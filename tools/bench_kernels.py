@@ -20,7 +20,7 @@ def run(shape, reps=10, faces=None):
     act = (ctypes.c_ubyte * 1)(0)
     s = torch.cuda.current_stream()
     for _ in range(3):
-        lib.psm_jacobi_sweep(dp.handle, act, 0.8, 0, ctypes.c_void_p(s.cuda_stream))
+        _lib.check(lib.psm_jacobi_sweep(dp.handle, act, 0.8, 0, ctypes.c_void_p(s.cuda_stream)))
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s)
