@@ -51,6 +51,10 @@ def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank, group=
     """Send ``send_lo`` to ``lo_rank`` and ``send_hi`` to ``hi_rank``; receive
     into ``recv_lo`` from ``lo_rank`` and ``recv_hi`` from ``hi_rank`` (None
     ranks are skipped).  Returns the list of outstanding requests."""
+    if send_lo.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo has no device-side point-to-point: stage through host memory
+        # (used to run the multi-process path with several ranks on one GPU)
+        return _exchange_via_host(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank, group)
     ops = []
     if lo_rank is not None:
         ops.append(dist.P2POp(dist.isend, send_lo, lo_rank, group))
@@ -61,6 +65,25 @@ def exchange_planes(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank, group=
     if not ops:
         return []
     return dist.batch_isend_irecv(ops)
+
+
+def _exchange_via_host(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank, group):
+    hs = {k: t.detach().cpu() for k, t in (("lo", send_lo), ("hi", send_hi))}
+    hr = {"lo": torch.empty(recv_lo.shape, dtype=recv_lo.dtype), "hi": torch.empty(recv_hi.shape, dtype=recv_hi.dtype)}
+    ops = []
+    if lo_rank is not None:
+        ops.append(dist.P2POp(dist.isend, hs["lo"], lo_rank, group))
+        ops.append(dist.P2POp(dist.irecv, hr["lo"], lo_rank, group))
+    if hi_rank is not None:
+        ops.append(dist.P2POp(dist.isend, hs["hi"], hi_rank, group))
+        ops.append(dist.P2POp(dist.irecv, hr["hi"], hi_rank, group))
+    for r in dist.batch_isend_irecv(ops) if ops else []:
+        r.wait()
+    if lo_rank is not None:
+        recv_lo.copy_(hr["lo"])
+    if hi_rank is not None:
+        recv_hi.copy_(hr["hi"])
+    return []
 
 
 def gather_plane_sums(local, group=None):
@@ -194,19 +217,32 @@ def dist_smooth(domain, config, cache, record_history=True):
         return [math.sqrt(v) for v in out.cpu().tolist()]
 
 
-def jacobi_step_overlapped(domain, dp, omega, slot):
+def jacobi_step_overlapped(domain, dp, omega, slot, events=None):
     """One line-Jacobi step of a slab with the halo exchange overlapped with
-    the interior sweep (see the module docstring)."""
+    the interior sweep (see the module docstring).  ``events``: optional list
+    collecting one list of (start, end) CUDA-event pairs per step, around the
+    sweep launches only (kernel time, not the halo)."""
     lib = _lib.load()
     p = domain.patch
     nzl = domain.nz_local
     act = (ctypes.c_ubyte * 1)(p._active)
     stream = ctypes.c_void_p(torch.cuda.current_stream(p.device).cuda_stream)
 
+    pairs = [] if events is not None else None
+    if events is not None:
+        events.append(pairs)
+
     def sweep(k0, k1):
         if k1 > k0:
+            if pairs is not None:
+                a = torch.cuda.Event(enable_timing=True)
+                a.record(torch.cuda.current_stream(p.device))
             _lib.check(lib.psm_jacobi_sweep_planes(dp.handle, act, float(omega), slot, 0, k0, k1, stream),
                        "jacobi_sweep_planes")
+            if pairs is not None:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record(torch.cuda.current_stream(p.device))
+                pairs.append((a, b))
 
     if domain.world == 1:
         sweep(0, nzl)
