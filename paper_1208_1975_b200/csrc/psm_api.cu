@@ -31,7 +31,7 @@ cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
                            cudaStream_t stream);
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
-                                   const long long* gprefix, long long total, int skip_x, cudaStream_t stream);
+                                   long long max_face, int skip_x, cudaStream_t stream);
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
                                     int ncopy, long long total, cudaStream_t stream);
 cudaError_t launch_plane_sums(const PatchDev* patches, int npatch, const double* partials, double* plane_sums,
@@ -324,6 +324,7 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     gpre[p] = g0;
     const long long px = d.nx + 2, py = d.ny + 2, pz = d.nz + 2;
     g0 += 2 * (py * pz + px * pz + px * py);
+    P->ghost_max_face = std::max(P->ghost_max_face, std::max(py * pz, std::max(px * pz, px * py)));
     const int nseg = (d.nx + kSeg - 1) / kSeg;
     smem = std::max(smem, (size_t)(h.R * row_stride(d.nx) + 2 * h.R * nseg) * sizeof(double));
   }
@@ -358,6 +359,7 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     }
     h.elem0 = e0;
     e0 += (long long)c.extent[0] * c.extent[1] * c.extent[2];
+    P->copy_max = std::max(P->copy_max, (long long)c.extent[0] * c.extent[1] * c.extent[2]);
   }
   P->copy_total = e0;
   cudaError_t err = cudaMalloc(&P->d_patches, npatch * sizeof(PatchDev));
@@ -476,12 +478,12 @@ int psm_refresh_ghosts(psm_plan* P, const unsigned char* active, int what, void*
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (what & PSM_GHOST_PHYSICAL) {
-    CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->d_gprefix, P->ghost_total,
+    CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->ghost_max_face,
                                     (what & PSM_GHOST_SKIP_X) ? 1 : 0, s));
     P->launches += P->ghost_total > 0;
   }
   if (what & PSM_GHOST_INTERFACE) {
-    CUDA_TRY(launch_interface_copies(P->d_patches, da, P->d_copies, P->ncopy, P->copy_total, s));
+    CUDA_TRY(launch_interface_copies(P->d_patches, da, P->d_copies, P->ncopy, P->copy_max, s));
     P->launches += (P->ncopy > 0 && P->copy_total > 0);
   }
   return PSM_OK;

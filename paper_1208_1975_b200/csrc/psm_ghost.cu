@@ -4,6 +4,8 @@
 //   fill_physical_ghosts       grid.py:311-330
 //   exchange_interface_ghosts  grid.py:523-547
 // and the summation of residual_norm (smoother.py:96-109).
+#include <algorithm>
+
 #include "psm_internal.cuh"
 
 namespace psm {
@@ -12,48 +14,42 @@ namespace psm {
 // reading the fresh x ghosts, then z), so every ghost cell ends up as
 // (-1)^(number of ghost coordinates) * u(nearest interior cell).  Computing
 // that closed form per cell gives the same bits with no pass ordering, so one
-// launch covers all faces of all patches.  Face counts per patch: 2*py*pz (x),
-// 2*px*pz (y), 2*px*py (z); edge cells are written by several faces with the
-// same value.  With skip_x the x faces are left to the Jacobi sweep, which
-// already stored them (their edges are rewritten by the y/z faces).
-__global__ void physical_ghost_kernel(const PatchDev* __restrict__ patches, int npatch,
-                                      const unsigned char* __restrict__ active,
-                                      const long long* __restrict__ gprefix, long long total, int skip_x) {
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
-       g += (long long)gridDim.x * blockDim.x) {
-    int lo = 0, hi = npatch - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (gprefix[mid] <= g) lo = mid; else hi = mid - 1;
-    }
-    const PatchDev& P = patches[lo];
-    double* u = P.buf[active[lo]];
-    const int px = P.nx + 2, py = P.ny + 2, pz = P.nz + 2;
-    long long c = g - gprefix[lo];
-    int i, j, k;
-    const long long nxf = 2LL * py * pz, nyf = 2LL * px * pz;
-    if (c < nxf) {
-      const int side = (int)(c / ((long long)py * pz));
-      const long long q = c - (long long)side * py * pz;
-      j = (int)(q % py);
-      k = (int)(q / py);
-      i = side ? px - 1 : 0;
-      if (skip_x && j > 0 && j < py - 1 && k > 0 && k < pz - 1) continue;
-    } else if (c < nxf + nyf) {
-      c -= nxf;
-      const int side = (int)(c / ((long long)px * pz));
-      const long long q = c - (long long)side * px * pz;
-      i = (int)(q % px);
-      k = (int)(q / px);
-      j = side ? py - 1 : 0;
+// launch covers all faces of all patches: grid (chunk, patch, face), 32-bit
+// index math, contiguous rows for the y and z faces.  Edge cells are written
+// by several faces with the same value.  With skip_x the x faces are left to
+// the Jacobi sweep, which already stored their interior; only their
+// perimeter (edges shared with y/z faces) is rewritten here.
+__global__ void __launch_bounds__(256) physical_ghost_kernel(const PatchDev* __restrict__ patches,
+                                                             const unsigned char* __restrict__ active, int skip_x,
+                                                             int pbase) {
+  const int face = blockIdx.z, axis = face >> 1, side = face & 1;
+  const int pi = pbase + blockIdx.y;
+  const PatchDev& P = patches[pi];
+  double* __restrict__ u = P.buf[active[pi]];
+  const int px = P.nx + 2, py = P.ny + 2, pz = P.nz + 2;
+  // face extent (A fastest, then B)
+  const int A = axis == 0 ? py : px, B = axis == 2 ? py : pz;
+  const bool perim = axis == 0 && skip_x;
+  const int n = perim ? 2 * A + 2 * (B - 2) : A * B;
+  for (int c = blockIdx.x * 1024 + threadIdx.x; c < min(n, (int)(blockIdx.x + 1) * 1024); c += 256) {
+    int a, b;
+    if (perim) {  // the face's border: rows b = 0 and B-1, then columns a = 0 and A-1
+      if (c < 2 * A) {
+        a = c % A;
+        b = c < A ? 0 : B - 1;
+      } else {
+        const int q = c - 2 * A;
+        a = (q & 1) ? A - 1 : 0;
+        b = 1 + (q >> 1);
+      }
     } else {
-      c -= nxf + nyf;
-      const int side = (int)(c / ((long long)px * py));
-      const long long q = c - (long long)side * px * py;
-      i = (int)(q % px);
-      j = (int)(q / px);
-      k = side ? pz - 1 : 0;
+      b = c / A;
+      a = c - b * A;
     }
+    int i, j, k;
+    if (axis == 0) { i = side ? px - 1 : 0; j = a; k = b; }
+    else if (axis == 1) { i = a; j = side ? py - 1 : 0; k = b; }
+    else { i = a; j = b; k = side ? pz - 1 : 0; }
     const int ic = min(max(i, 1), px - 2), jc = min(max(j, 1), py - 2), kc = min(max(k, 1), pz - 2);
     const int flips = (i != ic) + (j != jc) + (k != kc);
     const double val = u[(long long)ic + (long long)px * (jc + (long long)py * kc)];
@@ -63,30 +59,23 @@ __global__ void physical_ghost_kernel(const PatchDev* __restrict__ patches, int 
 
 // Interface ghosts: dst ghost layer <- src interior layer.  Sources are
 // interior cells and destinations ghost cells, so no copy reads what another
-// writes: the snapshot semantics of grid.py:530-546 hold in one launch.
-__global__ void interface_copy_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
-                                      const CopyDev* __restrict__ copies, int ncopy, long long total) {
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
-       g += (long long)gridDim.x * blockDim.x) {
-    int lo = 0, hi = ncopy - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (copies[mid].elem0 <= g) lo = mid; else hi = mid - 1;
-    }
-    const CopyDev& C = copies[lo];
-    const long long e = g - C.elem0;
-    const int a = (int)(e % C.ext[0]);
-    const long long t = e / C.ext[0];
-    const int b = (int)(t % C.ext[1]);
-    const int c = (int)(t / C.ext[1]);
-    const PatchDev& S = patches[C.src];
-    const PatchDev& D = patches[C.dst];
-    const double* su = S.buf[active[C.src]];
-    double* du = D.buf[active[C.dst]];
-    const long long spx = S.nx + 2, spy = S.ny + 2, dpx = D.nx + 2, dpy = D.ny + 2;
-    const long long si = (C.src_lo[0] + a + 1) + spx * ((C.src_lo[1] + b + 1) + spy * (C.src_lo[2] + c + 1));
-    const long long di = (C.dst_lo[0] + a + 1) + dpx * ((C.dst_lo[1] + b + 1) + dpy * (C.dst_lo[2] + c + 1));
-    du[di] = su[si];
+// writes: the snapshot semantics of grid.py:530-546 hold in one launch.  Grid
+// (chunk, copy), 32-bit index math, x fastest (contiguous runs).
+__global__ void __launch_bounds__(256) interface_copy_kernel(const PatchDev* __restrict__ patches,
+                                                             const unsigned char* __restrict__ active,
+                                                             const CopyDev* __restrict__ copies, int cbase) {
+  const CopyDev& C = copies[cbase + blockIdx.y];
+  const int e0 = C.ext[0], e01 = C.ext[0] * C.ext[1], n = e01 * C.ext[2];
+  const PatchDev& S = patches[C.src];
+  const PatchDev& D = patches[C.dst];
+  const double* __restrict__ su = S.buf[active[C.src]];
+  double* __restrict__ du = D.buf[active[C.dst]];
+  const long long spx = S.nx + 2, spy = S.ny + 2, dpx = D.nx + 2, dpy = D.ny + 2;
+  const long long sb = (C.src_lo[0] + 1) + spx * ((C.src_lo[1] + 1) + spy * (C.src_lo[2] + 1));
+  const long long db = (C.dst_lo[0] + 1) + dpx * ((C.dst_lo[1] + 1) + dpy * (C.dst_lo[2] + 1));
+  for (int e = blockIdx.x * 1024 + threadIdx.x; e < min(n, (int)(blockIdx.x + 1) * 1024); e += 256) {
+    const int c = e / e01, r = e - c * e01, b = r / e0, a = r - b * e0;
+    du[db + a + dpx * (b + dpy * c)] = su[sb + a + spx * (b + spy * c)];
   }
 }
 
@@ -152,23 +141,25 @@ cudaError_t launch_halo_unpack(double* dst_plane, const double* src_plane, int p
   return cudaGetLastError();
 }
 
+// max_face: largest face (cells) of any patch; 1024 cells per CTA
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
-                                   const long long* gprefix, long long total, int skip_x, cudaStream_t stream) {
-  if (total == 0) return cudaSuccess;
-  const int tpb = 256;
-  long long blocks = (total + tpb - 1) / tpb;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  physical_ghost_kernel<<<(unsigned)blocks, tpb, 0, stream>>>(patches, npatch, active, gprefix, total, skip_x);
+                                   long long max_face, int skip_x, cudaStream_t stream) {
+  if (npatch == 0 || max_face == 0) return cudaSuccess;
+  for (int base = 0; base < npatch; base += 65535) {
+    const dim3 grid((unsigned)((max_face + 1023) / 1024), (unsigned)std::min(65535, npatch - base), 6);
+    physical_ghost_kernel<<<grid, 256, 0, stream>>>(patches, active, skip_x, base);
+  }
   return cudaGetLastError();
 }
 
+// max_elems: largest copy (cells)
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
-                                    int ncopy, long long total, cudaStream_t stream) {
-  if (total == 0 || ncopy == 0) return cudaSuccess;
-  const int tpb = 256;
-  long long blocks = (total + tpb - 1) / tpb;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  interface_copy_kernel<<<(unsigned)blocks, tpb, 0, stream>>>(patches, active, copies, ncopy, total);
+                                    int ncopy, long long max_elems, cudaStream_t stream) {
+  if (max_elems == 0 || ncopy == 0) return cudaSuccess;
+  for (int base = 0; base < ncopy; base += 65535) {
+    const dim3 grid((unsigned)((max_elems + 1023) / 1024), (unsigned)std::min(65535, ncopy - base), 1);
+    interface_copy_kernel<<<grid, 256, 0, stream>>>(patches, active, copies, base);
+  }
   return cudaGetLastError();
 }
 

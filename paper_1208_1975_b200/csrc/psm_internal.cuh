@@ -146,6 +146,8 @@ struct psm_plan {
   long long copy_total = 0;
   long long* d_gprefix = nullptr;
   long long ghost_total = 0;
+  long long ghost_max_face = 0;  // largest face of any patch (ghost kernel grid)
+  long long copy_max = 0;        // largest interface copy (copy kernel grid)
   long long ntiles = 0;
   int nplanes = 0;
   int threads = 256;
