@@ -40,7 +40,10 @@
 
 namespace psm {
 
-constexpr int kBandT = 64;  // threads per plane CTA
+#ifndef PSM_BAND_T
+#define PSM_BAND_T 64
+#endif
+constexpr int kBandT = PSM_BAND_T;  // threads per plane CTA
 
 __device__ __forceinline__ void band_cp8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
@@ -105,7 +108,7 @@ __device__ __forceinline__ void band_conv_row(const double* __restrict__ e, cons
 }
 
 template <int K, int BW>
-__global__ void __launch_bounds__(kBandT, 6) plane_band_jacobi_kernel(const PatchDev* __restrict__ patches,
+__global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel(const PatchDev* __restrict__ patches,
                                                                   const unsigned char* __restrict__ active,
                                                                   double omega, const double* __restrict__ rbuf,
                                                                   double* __restrict__ zbuf,
@@ -262,12 +265,9 @@ static cudaError_t band_launch_t(const PatchDev* patches, const unsigned char* a
   return cudaGetLastError();
 }
 
-int band_k_for(int nx) {
-  if (nx <= 64) return 1;
-  if (nx <= 128) return 2;
-  if (nx <= 256) return 4;
-  if (nx <= 512) return 8;
-  if (nx <= 1024) return 16;
+int band_k_for(int nx) {  // outputs per thread: kBandT * K >= nx
+  for (int k = 1; k <= 16; k *= 2)
+    if (nx <= kBandT * k) return k;
   return 0;
 }
 
