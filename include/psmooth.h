@@ -37,7 +37,7 @@ enum psm_status {
   PSM_EUNSUPPORTED = -5
 };
 
-enum psm_block_kind { PSM_BLOCK_LINE = 1, PSM_BLOCK_PLANE = 2 };
+enum psm_block_kind { PSM_BLOCK_LINE = 1, PSM_BLOCK_PLANE = 2, PSM_BLOCK_BOX = 3 };
 
 enum psm_gs_mode {
   PSM_GS_WAVEFRONT = 0, /* deterministic: == lexicographic block GS (runtime.py:164-168) */
@@ -74,6 +74,13 @@ int psm_version(void);
  *      blocklinalg.py:50-87).  One object per block shape; built once,
  *      outside any timed region.  line: extent (nx,1,1); plane: (nx,ny,1). */
 int psm_factors_create(int kind, const psm_stencil* st, int nx, int ny, psm_factors** out);
+/* Box blocks (ex, ey, ez), every extent in [1, 8] (the paper's cubic blocks,
+ * DEFAULT_BLOCK_SIZES analysis.py:38-46): separable exact inverse
+ * D Q Lambda^-1 Q D^-1 (per-axis DST-I with a diagonal similarity for
+ * non-symmetric faces of one sign); blocks truncated at patch edges use the
+ * same tables.  Replaces invert_dense + matvec (blocklinalg.py:50-105) for
+ * them.  PSM_EUNSUPPORTED for faces of opposite signs on one axis. */
+int psm_factors_create_box(const psm_stencil* st, int ex, int ey, int ez, psm_factors** out);
 int psm_factors_destroy(psm_factors* fac);
 /* Apply the exact block inverse to `count` contiguous blocks of r (device),
  * writing x (device): the block_update matvec of blocklinalg.py:90-105

@@ -4,7 +4,7 @@ TEST INFRASTRUCTURE ONLY.  Run in the dev container, where the read-only
 reference lives at /root/reference (it does not exist on the GPU box, so the
 outputs are committed as small fixtures):
 
-    python oracle/make_golden.py
+    python oracle/make_golden.py [--only-box]
 
 Every case builds its inputs with seeded numpy generators, runs
 ``patchsmooth.smooth`` (``/root/reference/pkg/src/patchsmooth/smoother.py:197``)
@@ -162,8 +162,28 @@ def host_logic_case(ps):
     _save("host_logic", **out)
 
 
+def box_cases(ps):
+    """Box blocks (the paper's cubic blocks, DEFAULT_BLOCK_SIZES), including
+    blocks truncated at patch edges and x-segments shorter than the line."""
+    for scheme in ("block_jacobi", "chaotic_block_gs"):
+        tag = "jac" if scheme == "block_jacobi" else "gs"
+        random_patch_case(ps, f"box_{tag}_16x12x10_b4x4x4", (16, 12, 10), (4, 4, 4), scheme, 2, seed=21)
+        random_patch_case(ps, f"box_{tag}_8x8x8_b2x2x2", (8, 8, 8), (2, 2, 2), scheme, 3, seed=22)
+        random_patch_case(ps, f"box_{tag}_17x9x11_b8x8x8", (17, 9, 11), (8, 8, 8), scheme, 2, seed=23)
+        random_patch_case(ps, f"box_{tag}_aniso_12x8x6_b4x2x2", (12, 8, 6), (4, 2, 2), scheme, 2, seed=24,
+                          stencil="aniso_line")
+        random_patch_case(ps, f"box_{tag}_12x10x8_b8x1x1", (12, 10, 8), (8, 1, 1), scheme, 2, seed=25)
+        multipatch_case(ps, f"multi_box_{tag}_2x2x2_of_8", (2, 2, 2), (8, 8, 8), (4, 4, 4), scheme, 2)
+    random_patch_case(ps, "box_jac_w06_10x10x10_b4x4x4", (10, 10, 10), (4, 4, 4), "block_jacobi", 2, omega=0.6,
+                      seed=26)
+    random_patch_case(ps, "box_gs_9x9x9_b3x3x3", (9, 9, 9), (3, 3, 3), "chaotic_block_gs", 3, seed=27)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--only-box" in sys.argv:
+        box_cases(_ref())
+        return
     ps = _ref()
     t0 = time.perf_counter()
     # single patch, random u and f
@@ -192,6 +212,7 @@ def main():
         multipatch_case(ps, f"multi_line_{tag}_3x1x2_of_32x4x3", (3, 1, 2), (32, 4, 3), (32, 1, 1), scheme, 2)
         zsplit_case(ps, f"zsplit_line_{tag}_32x8x8_in4", (32, 8, 8), 4, (32, 1, 1), scheme, 3)
     zsplit_case(ps, "zsplit_plane_jac_8x8x8_in2", (8, 8, 8), 2, (8, 8, 1), "block_jacobi", 2)
+    box_cases(ps)
     host_logic_case(ps)
     # the CLI's own inputs (seed 42, f = 0) -- SURVEY section 8c golden histories
     seeded_case(ps, "seeded_line_jac_64", (64, 64, 64), (64, 1, 1), "block_jacobi", 10, (0, 31, 63))

@@ -273,12 +273,63 @@ def _is_plane(dims, block):
 
 
 def block_kind(dims, block):
-    """Classify degenerate block_dims (grid.py:298-306 truncation)."""
+    """Classify block_dims (grid.py:298-306 truncation): one block per line,
+    per plane, or general boxes (the paper's cubic blocks)."""
     if _is_line(dims, block):
         return "line"
     if _is_plane(dims, block):
         return "plane"
-    raise ValueError(f"block {block} is neither a line nor a plane block for {dims}")
+    return "box"
+
+
+def box_matrix(ext, center=DEFAULT_CENTER, faces=DEFAULT_FACES):
+    """assemble_block_matrix (stencil.py:115-138): the closure-free operator of
+    one block, cells x fastest; couplings leaving the block are dropped."""
+    ex, ey, ez = ext
+    n = ex * ey * ez
+    a = np.zeros((n, n))
+    for k in range(ez):
+        for j in range(ey):
+            for i in range(ex):
+                row = i + ex * (j + ey * k)
+                a[row, row] = center
+                for coef, (dx, dy, dz) in zip(faces, FACE_OFFSETS):
+                    ii, jj, kk = i + dx, j + dy, k + dz
+                    if 0 <= ii < ex and 0 <= jj < ey and 0 <= kk < ez:
+                        a[row, ii + ex * (jj + ey * kk)] = coef
+    return a
+
+
+_BOX_INV = {}
+
+
+def box_inverse(ext, center=DEFAULT_CENTER, faces=DEFAULT_FACES):
+    """Dense exact inverse per block shape (invert_dense, blocklinalg.py:50-87)."""
+    key = (tuple(ext), float(center), tuple(float(f) for f in faces))
+    inv = _BOX_INV.get(key)
+    if inv is None:
+        inv = np.linalg.inv(box_matrix(ext, center, faces))
+        _BOX_INV[key] = inv
+    return inv
+
+
+def box_ranges(dims, block):
+    """decompose_blocks (grid.py:286-308): lexicographic, x fastest."""
+    counts = [-(-n // b) for n, b in zip(dims, block)]
+    for kz in range(counts[2]):
+        for ky in range(counts[1]):
+            for kx in range(counts[0]):
+                lo = (kx * block[0], ky * block[1], kz * block[2])
+                yield lo, tuple(min(b, n - l) for b, n, l in zip(block, dims, lo))
+
+
+def box_update(p, lo, ext, omega, center, faces, dst):
+    """block_update (smoother.py:90-93) of one box: dst_b = u_b + omega Ainv r_b
+    with r_b = block_residual of the current u (cells x fastest)."""
+    r = residual(p.u, p.f, center, faces, lo=lo, ext=ext)
+    x = box_inverse(ext, center, faces) @ r.transpose(2, 1, 0).ravel()
+    sl = tuple(slice(l + 1, l + e + 1) for l, e in zip(lo, ext))
+    dst[sl] = p.u[sl] + omega * x.reshape(ext[2], ext[1], ext[0]).transpose(2, 1, 0)
 
 
 # --------------------------------------------------------------------------
@@ -289,6 +340,10 @@ def jacobi_step(level, block, omega, center=DEFAULT_CENTER, faces=DEFAULT_FACES)
     then swap buffers and refresh ghosts."""
     for p in level.patches:
         kind = block_kind(p.dims, block)
+        if kind == "box":
+            for lo, ext in box_ranges(p.dims, block):
+                box_update(p, lo, ext, omega, center, faces, p.other)
+            continue
         r = residual(p.u, p.f, center, faces)
         x = line_solve(r, center, faces) if kind == "line" else plane_solve(r, center, faces)
         p.other[1:-1, 1:-1, 1:-1] = p.interior + omega * x
@@ -307,6 +362,10 @@ def gs_step(level, block, omega, center=DEFAULT_CENTER, faces=DEFAULT_FACES):
         kind = block_kind(p.dims, block)
         nx, ny, nz = p.dims
         u = p.u
+        if kind == "box":  # lexicographic blocks, in place
+            for lo, ext in box_ranges(p.dims, block):
+                box_update(p, lo, ext, omega, center, faces, u)
+            continue
         if kind == "plane":
             for k in range(nz):
                 r = residual(u, p.f, center, faces, lo=(0, 0, k), ext=(nx, ny, 1))

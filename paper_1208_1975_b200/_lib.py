@@ -23,6 +23,7 @@ PSM_EUNSUPPORTED = -5
 
 BLOCK_LINE = 1
 BLOCK_PLANE = 2
+BLOCK_BOX = 3
 GHOST_PHYSICAL = 1
 GHOST_INTERFACE = 2
 GHOST_SKIP_X = 4
@@ -35,6 +36,7 @@ EXPORTS = (
     "psm_last_error",
     "psm_version",
     "psm_factors_create",
+    "psm_factors_create_box",
     "psm_factors_destroy",
     "psm_factors_apply",
     "psm_plan_create",
@@ -109,6 +111,7 @@ def load():
             "psm_last_error": (ctypes.c_char_p, []),
             "psm_version": (i, []),
             "psm_factors_create": (i, [i, ctypes.POINTER(Stencil), i, i, ctypes.POINTER(vp)]),
+            "psm_factors_create_box": (i, [ctypes.POINTER(Stencil), i, i, i, ctypes.POINTER(vp)]),
             "psm_factors_destroy": (i, [vp]),
             "psm_factors_apply": (i, [vp, vp, vp, ll, vp]),
             "psm_plan_create": (

@@ -46,20 +46,26 @@ class SingularMatrixError(ValueError):
 
 
 def block_kind(extent):
-    """'line' for (n,1,1), 'plane' for (nx,ny,1) with ny > 1, else ValueError."""
+    """The natural device form of a block extent: 'line' for (n,1,1), 'plane'
+    for (nx,ny,1) with ny > 1, 'box' for other blocks with at most 8 cells per
+    axis; ValueError otherwise."""
     ex, ey, ez = _int3(extent, "extent")
     if min(ex, ey, ez) < 1:
         raise ValueError(f"extent must be positive, got {(ex, ey, ez)}")
-    if ez != 1:
-        raise ValueError(
-            f"block extent {(ex, ey, ez)} is not a line (nx,1,1) or plane (nx,ny,1) block; "
-            "the device smoother implements line and plane blocks"
-        )
-    return "line" if ey == 1 else "plane"
+    if ez == 1:
+        return "line" if ey == 1 else "plane"
+    if max(ex, ey, ez) <= 8:
+        return "box"
+    raise ValueError(
+        f"block extent {(ex, ey, ez)} is not a line (nx,1,1), plane (nx,ny,1) or box (<= 8 per axis) block; "
+        "the device smoother implements those"
+    )
 
 
 class BlockFactors:
-    """Device tables of one exact block inverse (line or plane)."""
+    """Device tables of one exact block inverse.  The natural form (see
+    ``block_kind``) is built eagerly; a plan may also ask for the box form of
+    a line or plane extent (the same inverse, applied by the box kernel)."""
 
     def __init__(self, stencil, extent, device):
         self.extent = _int3(extent, "extent")
@@ -68,14 +74,29 @@ class BlockFactors:
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise RuntimeError("block factors live on a CUDA device; there is no CPU fallback")
+        self._handles = {}
+        self.handle = self.handle_for(self.kind)
+
+    def handle_for(self, kind):
+        """The C factor handle of this inverse in form ``kind``."""
+        h = self._handles.get(kind)
+        if h is not None:
+            return h
         lib = _lib.load()
-        h = ctypes.c_void_p()
-        kind = _lib.BLOCK_LINE if self.kind == "line" else _lib.BLOCK_PLANE
-        st = stencil._cstruct()
+        out = ctypes.c_void_p()
+        st = self.stencil._cstruct()
         with torch.cuda.device(self.device):
-            _lib.check(lib.psm_factors_create(kind, ctypes.byref(st), self.extent[0], self.extent[1],
-                                              ctypes.byref(h)), "psm_factors_create")
-        self.handle = h.value
+            if kind == "box":
+                if max(self.extent) > 8:
+                    raise ValueError(f"box blocks need at most 8 cells per axis, got {self.extent}")
+                _lib.check(lib.psm_factors_create_box(ctypes.byref(st), *self.extent, ctypes.byref(out)),
+                           "psm_factors_create_box")
+            else:
+                ck = _lib.BLOCK_LINE if kind == "line" else _lib.BLOCK_PLANE
+                _lib.check(lib.psm_factors_create(ck, ctypes.byref(st), self.extent[0], self.extent[1],
+                                                  ctypes.byref(out)), "psm_factors_create")
+        self._handles[kind] = out.value
+        return out.value
 
     @property
     def order(self):
@@ -106,13 +127,13 @@ class BlockFactors:
         return self.apply(eye).T.contiguous()
 
     def __del__(self):
-        h = getattr(self, "handle", None)
-        if h:
+        for h in getattr(self, "_handles", {}).values():
             try:
                 _lib.load().psm_factors_destroy(h)
             except Exception:
                 pass
-            self.handle = None
+        self._handles = {}
+        self.handle = None
 
     def __repr__(self):
         return f"BlockFactors({self.kind} {self.extent})"

@@ -78,6 +78,14 @@ int psm_plane_plan_setup(psm_plan* plan);  // psm_plane.cu
 int psm_plane_plan_free(psm_plan* plan);
 int psm_plane_jacobi(psm_plan* P, const unsigned char* d_active, double omega, double* partials, cudaStream_t s);
 int psm_plane_gs(psm_plan* P, const unsigned char* d_active, double omega, cudaStream_t s);
+// box path (psm_box.cu)
+int psm_box_build(const psm_stencil* st, int ex, int ey, int ez, psm_factors* F);
+namespace psm {
+cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* active, const StencilDev& st,
+                             double omega, const int4* blocks, int nblocks, int inplace, int mx, int my, int mz,
+                             int bx, int by, int bz, cudaStream_t s);
+cudaError_t launch_box_apply(const BoxFac* F, const double* r, double* x, long long count, cudaStream_t s);
+}
 extern int psm_plane_band_mode;  // psm_plane.cu
 // pipelined line GS (psm_line_gs_pipe.cu)
 bool gs_pipe_supported(int nx);
@@ -231,6 +239,31 @@ int psm_factors_create(int kind, const psm_stencil* st, int nx, int ny, psm_fact
   return PSM_OK;
 }
 
+int psm_factors_create_box(const psm_stencil* st, int ex, int ey, int ez, psm_factors** out) {
+  if (!st || !out) return fail(PSM_EINVAL, "null argument");
+  *out = nullptr;
+  if (!(st->center > 0) || !isfinite(st->center)) return fail(PSM_EINVAL, "center must be positive and finite");
+  for (int i = 0; i < 6; ++i)
+    if (!isfinite(st->faces[i])) return fail(PSM_EINVAL, "face coefficients must be finite");
+  if (ex < 1 || ey < 1 || ez < 1) return fail(PSM_EINVAL, "block extent must be positive, got (%d,%d,%d)", ex, ey, ez);
+  psm_factors* F = new psm_factors();
+  memset(F, 0, sizeof *F);
+  F->kind = PSM_BLOCK_BOX;
+  F->nx = ex;
+  F->ny = ey;
+  F->nz = ez;
+  F->center = st->center;
+  memcpy(F->faces, st->faces, sizeof F->faces);
+  const int rc = psm_box_build(st, ex, ey, ez, F);
+  if (rc != PSM_OK) {
+    if (F->dev) cudaFree(F->dev);
+    delete F;
+    return rc;
+  }
+  *out = F;
+  return PSM_OK;
+}
+
 int psm_factors_destroy(psm_factors* F) {
   if (!F) return PSM_OK;
   if (F->dev) cudaFree(F->dev);
@@ -243,6 +276,10 @@ int psm_factors_apply(const psm_factors* F, const double* r, double* x, long lon
   if (!F || !r || !x || count < 0) return fail(PSM_EINVAL, "bad arguments to psm_factors_apply");
   if (F->kind == PSM_BLOCK_LINE) {
     CUDA_TRY(launch_line_apply(F->d_line, r, x, count, (cudaStream_t)stream));
+    return PSM_OK;
+  }
+  if (F->kind == PSM_BLOCK_BOX) {
+    CUDA_TRY(launch_box_apply(F->d_box, r, x, count, (cudaStream_t)stream));
     return PSM_OK;
   }
   return psm_plane_apply(F, r, x, count, (cudaStream_t)stream);
@@ -265,7 +302,8 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
   if (!patches || npatch < 1) return fail(PSM_EINVAL, "a plan needs at least one patch");
   if (ncopy < 0 || (ncopy > 0 && !copies)) return fail(PSM_EINVAL, "bad interface copy list");
   if (!st) return fail(PSM_EINVAL, "null stencil");
-  if (kind != 0 && kind != PSM_BLOCK_LINE && kind != PSM_BLOCK_PLANE) return fail(PSM_EINVAL, "bad kind %d", kind);
+  if (kind != 0 && kind != PSM_BLOCK_LINE && kind != PSM_BLOCK_PLANE && kind != PSM_BLOCK_BOX)
+    return fail(PSM_EINVAL, "bad kind %d", kind);
   psm_plan* P = new psm_plan();
   P->npatch = npatch;
   P->ncopy = ncopy;
@@ -282,7 +320,8 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     if (kind != 0) {
       psm_factors* F = fac ? fac[p] : nullptr;
       if (!F || F->kind != kind) { delete P; return fail(PSM_EINVAL, "patch %d lacks matching factors", p); }
-      if (F->nx != d.nx || (kind == PSM_BLOCK_PLANE && F->ny != d.ny)) {
+      if ((kind != PSM_BLOCK_BOX && F->nx != d.nx) || (kind == PSM_BLOCK_PLANE && F->ny != d.ny) ||
+          (kind == PSM_BLOCK_BOX && (F->nx > d.nx || F->ny > d.ny || F->nz > d.nz))) {
         delete P;
         return fail(PSM_EINVAL, "patch %d factors are for another block shape", p);
       }
@@ -317,6 +356,7 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     h.plane0 = plane0;
     h.lf = (kind == PSM_BLOCK_LINE) ? P->fac[p]->d_line : nullptr;
     h.pf = (kind == PSM_BLOCK_PLANE) ? P->fac[p]->d_plane : nullptr;
+    h.bf = (kind == PSM_BLOCK_BOX) ? P->fac[p]->d_box : nullptr;
     h.cell0 = cell0;
     cell0 += (long long)d.nx * d.ny * d.nz;
     tile0 += h.tiles;
@@ -376,6 +416,59 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     psm_plan_destroy(P);
     return fail(PSM_ECUDA, "plan setup: %s", cudaGetErrorString(err));
   }
+  if (kind == PSM_BLOCK_BOX) {  // block list, wavefront-major (bi + bj + bk), then patch, then lexicographic
+    std::vector<std::vector<int>> waves;
+    for (int p = 0; p < npatch; ++p) {
+      const psm_factors* F = P->fac[p];
+      const PatchDev& h = P->hp[p];
+      const int cx = (h.nx + F->nx - 1) / F->nx, cy = (h.ny + F->ny - 1) / F->ny, cz = (h.nz + F->nz - 1) / F->nz;
+      for (int bk = 0; bk < cz; ++bk)
+        for (int bj = 0; bj < cy; ++bj)
+          for (int bi = 0; bi < cx; ++bi) {
+            const int w = bi + bj + bk;
+            if ((int)waves.size() <= w) waves.resize(w + 1);
+            waves[w].insert(waves[w].end(), {p, bi * F->nx, bj * F->ny, bk * F->nz});
+          }
+    }
+    std::vector<int> all;
+    P->box_wave_off.assign(1, 0);
+    for (auto& w : waves) {
+      all.insert(all.end(), w.begin(), w.end());
+      P->box_wave_off.push_back((int)(all.size() / 4));
+    }
+    P->nboxes = (int)(all.size() / 4);
+    // Jacobi regions: (8/b) blocks per axis (all patches share block dims up
+    // to truncation: use the first patch's; truncated patches just clip)
+    const psm_factors* F0 = P->fac[0];
+    bool same = true;
+    for (int p = 1; p < npatch; ++p) same = same && P->fac[p]->nx == F0->nx && P->fac[p]->ny == F0->ny &&
+                                               P->fac[p]->nz == F0->nz;
+    P->box_dims[0] = same ? F0->nx : 0;
+    P->box_dims[1] = same ? F0->ny : 0;
+    P->box_dims[2] = same ? F0->nz : 0;
+    P->reg_m[0] = same ? std::max(1, 8 / F0->nx) : 1;
+    P->reg_m[1] = same ? std::max(1, 8 / F0->ny) : 1;
+    P->reg_m[2] = same ? std::max(1, 8 / F0->nz) : 1;
+    std::vector<int> regs;
+    for (int p = 0; p < npatch; ++p) {
+      const psm_factors* F = P->fac[p];
+      const PatchDev& h = P->hp[p];
+      const int Rx = F->nx * P->reg_m[0], Ry = F->ny * P->reg_m[1], Rz = F->nz * P->reg_m[2];
+      for (int z = 0; z < h.nz; z += Rz)
+        for (int y = 0; y < h.ny; y += Ry)
+          for (int x = 0; x < h.nx; x += Rx) regs.insert(regs.end(), {p, x, y, z});
+    }
+    P->nregions = (int)(regs.size() / 4);
+    cudaError_t e = cudaMalloc(&P->d_boxes, std::max<size_t>(16, all.size() * sizeof(int)));
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_boxes, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_box_regions, std::max<size_t>(16, regs.size() * sizeof(int)));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(P->d_box_regions, regs.data(), regs.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      psm_plan_destroy(P);
+      return fail(PSM_ECUDA, "box block list: %s", cudaGetErrorString(e));
+    }
+  }
   if (kind == PSM_BLOCK_PLANE) {
     int rc = psm_plane_plan_setup(P);
     if (rc != PSM_OK) {
@@ -400,6 +493,8 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_unit_patch);
   cudaFree(P->d_unit_plane);
   cudaFree(P->d_gsflags);
+  cudaFree(P->d_boxes);
+  cudaFree(P->d_box_regions);
   psm_gs_pipe_free(P);
   for (auto& kv : P->unit_cache) cudaFree(kv.second.first);
   for (auto& kv : P->active_cache) cudaFree(kv.second);
@@ -635,6 +730,21 @@ int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int
   cudaStream_t s = (cudaStream_t)stream;
   if (P->kind == PSM_BLOCK_LINE) return sweep_planes(P, da, omega, part, 0, P->npatch, 0, -1, s);
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_jacobi(P, da, omega, part, s);
+  if (P->kind == PSM_BLOCK_BOX) {
+    if (slot >= 0) {  // history entry of the current iterate (tile partials)
+      if (P->tiled) {
+        CUDA_TRY(launch_line_tiles(0, P->d_patches, P->npatch, da, P->st, 0.0, part, nullptr, 0, P->ntiles,
+                                   P->threads, 0, s));
+      } else {
+        CUDA_TRY(launch_line_generic(0, P->d_patches, P->npatch, da, P->st, 0.0, part, 0, P->ntiles, s));
+      }
+      P->launches += 1;
+    }
+    CUDA_TRY(launch_box_sweep(P->d_patches, da, P->st, omega, P->d_box_regions, P->nregions, 0, P->reg_m[0],
+                              P->reg_m[1], P->reg_m[2], P->box_dims[0], P->box_dims[1], P->box_dims[2], s));
+    P->launches += 1;
+    return PSM_OK;
+  }
   return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
 }
 
@@ -810,6 +920,15 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_gs(P, da, omega, s);
+  if (P->kind == PSM_BLOCK_BOX) {  // lexicographic block order = wavefronts bi+bj+bk, in place
+    for (size_t w = 0; w + 1 < P->box_wave_off.size(); ++w) {
+      const int b0 = P->box_wave_off[w], b1 = P->box_wave_off[w + 1];
+      CUDA_TRY(launch_box_sweep(P->d_patches, da, P->st, omega, P->d_boxes + b0, b1 - b0, 1, 1, 1, 1,
+                                P->box_dims[0], P->box_dims[1], P->box_dims[2], s));
+      P->launches += 1;
+    }
+    return PSM_OK;
+  }
   if (P->kind != PSM_BLOCK_LINE) return fail(PSM_EINVAL, "plan was created without a block kind (ghost-only)");
   bool pipe = true;
   for (auto& h : P->hp)  // TMA row copies need 16-byte aligned buffers

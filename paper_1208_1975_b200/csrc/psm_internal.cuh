@@ -50,6 +50,18 @@ struct PlaneFac {
   const double* H;     // [nj+1][bw+1] symmetric kernels H_j(0..bw)
 };
 
+// Box-block tables (psm_box.cu): per axis a and extent e in 1..8, forward
+// F = Q diag(s^-p), backward B = diag(s^p) Q (8x8 row-major) and the eigen
+// components L; the block's eigenvalue is c + Lx[i] + Ly[j] + Lz[k].
+struct BoxFac {
+  const double* F;
+  const double* B;
+  const double* L;
+  const double* IL;  // 1/lambda per (ex, ey, ez) in [1,8]^3: [((ex-1)*8+ey-1)*8+ez-1][k][j][i] (stride 8)
+  double c;
+  int bx, by, bz;  // block dims (already truncated to the patch)
+};
+
 struct PatchDev {
   double* buf[2];
   const double* f;
@@ -62,6 +74,7 @@ struct PatchDev {
   long long cell0;  // first interior cell (prefix of nx*ny*nz), for plane workspaces
   const LineFac* lf;
   const PlaneFac* pf;
+  const BoxFac* bf;
 };
 
 struct CopyDev {
@@ -131,8 +144,11 @@ struct psm_factors {
   void* dev;            // one allocation: struct + tables
   psm::LineFac* d_line;      // kind == line
   psm::PlaneFac* d_plane;    // kind == plane
+  psm::BoxFac* d_box;        // kind == box
   psm::LineFac h_line;       // host copy (pointers refer to device memory)
   psm::PlaneFac h_plane;
+  psm::BoxFac h_box;
+  int nz;                    // box blocks: ez
   double center, faces[6];
 };
 
@@ -173,6 +189,14 @@ struct psm_plan {
   GsPipeState* gspipe = nullptr;
   int* d_gsflags = nullptr;  // nplanes progress words + one ticket per group
   int gs_ntickets = 0;
+  // box path: blocks (patch, x0, y0, z0) sorted by wavefront bi+bj+bk (GS),
+  // and Jacobi regions of (8/bx) x (8/by) x (8/bz) blocks
+  int4* d_boxes = nullptr;
+  int nboxes = 0;
+  int4* d_box_regions = nullptr;
+  int nregions = 0, reg_m[3] = {1, 1, 1};
+  int box_dims[3] = {0, 0, 0};  // common block dims of all patches (0: they differ)
+  std::vector<int> box_wave_off;  // blocks of wavefront w: [off[w], off[w+1])
   // plane path
   PlaneState* plane = nullptr;
   // CUDA graphs of whole smooth() step sequences (psm_smooth_steps)

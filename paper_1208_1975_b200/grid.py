@@ -470,7 +470,8 @@ class _DevicePlan:
         nc = len(level.adjacency)
         cd = (_lib.CopyDesc * max(1, nc))(*[c._desc() for c in level.adjacency])
         st = stencil._cstruct()
-        fac = (ctypes.c_void_p * n)(*[f.handle for f in factors]) if factors else None
+        kname = {_lib.BLOCK_LINE: "line", _lib.BLOCK_PLANE: "plane", _lib.BLOCK_BOX: "box"}.get(kind)
+        fac = (ctypes.c_void_p * n)(*[f.handle_for(kname) for f in factors]) if factors else None
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _lib.check(lib.psm_plan_create(pd, n, cd, nc, ctypes.byref(st), kind, fac, ctypes.byref(handle)),

@@ -83,20 +83,25 @@ class SmootherConfig:
 
 
 def block_shape_of(dims, block_dims):
-    """(extent, kind) when block_dims make one block per x-line ('line':
-    (>=nx,1,1)) or per xy-plane ('plane': (>=nx,>=ny,1)) of the patch, after
-    the reference's truncation (grid.py:298-306); ValueError otherwise.  A
-    plane block on a ny == 1 patch is a line block."""
+    """(extent, kind) of the blocks block_dims make on the patch, after the
+    reference's truncation (grid.py:298-306): 'line' for one block per x-line
+    ((>=nx,1,1)), 'plane' for one per xy-plane ((>=nx,>=ny,1)), 'box' for
+    blocks of at most 8 cells per axis (the paper's cubic blocks, truncated at
+    the patch edges by the kernel); ValueError otherwise.  A plane block on a
+    ny == 1 patch is a line block."""
     b = _int3(block_dims, "block_dims")
-    nx, ny, _ = dims.shape
+    nx, ny, nz = dims.shape
     if b[0] >= nx and b[2] == 1:
         if b[1] == 1 or ny == 1 and b[1] >= 1:
             return (nx, 1, 1), "line"
         if b[1] >= ny:
             return (nx, ny, 1), "plane"
+    ext = (min(b[0], nx), min(b[1], ny), min(b[2], nz))
+    if max(ext) <= 8:
+        return ext, "box"
     raise ValueError(
-        f"block_dims {b} on a {dims.shape} patch are neither line blocks (>=nx,1,1) nor plane "
-        "blocks (>=nx,>=ny,1); the device smoother implements exactly those"
+        f"block_dims {b} on a {dims.shape} patch are neither line blocks (>=nx,1,1), plane blocks "
+        "(>=nx,>=ny,1) nor box blocks of at most 8 cells per axis; the device smoother implements exactly those"
     )
 
 
@@ -113,9 +118,9 @@ class _Plan:
             kinds.add(kind)
             factors.append(cache.get(config.stencil, ext, dev))
         if len(kinds) != 1:
-            raise ValueError(f"block_dims {config.block_dims} make mixed line/plane blocks on this level")
+            raise ValueError(f"block_dims {config.block_dims} make mixed line/plane/box blocks on this level")
         self.kind = kinds.pop()
-        ckind = _lib.BLOCK_LINE if self.kind == "line" else _lib.BLOCK_PLANE
+        ckind = {"line": _lib.BLOCK_LINE, "plane": _lib.BLOCK_PLANE, "box": _lib.BLOCK_BOX}[self.kind]
         self.dev = level._device_plan(ckind, config.stencil, factors)
         self.device = dev
 

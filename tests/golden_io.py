@@ -22,7 +22,7 @@ def names(prefix=""):
 
 
 def single_patch_cases():
-    return [n for n in names() if n.startswith(("line_", "plane_"))]
+    return [n for n in names() if n.startswith(("line_", "plane_", "box_"))]
 
 
 def multipatch_cases():

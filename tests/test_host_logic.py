@@ -105,14 +105,18 @@ def test_decompose_blocks_truncation():
         ((16, 16, 4), (16, 16, 1), ((16, 16, 1), "plane")),
         ((16, 16, 4), (32, 32, 1), ((16, 16, 1), "plane")),
         ((16, 1, 4), (16, 16, 1), ((16, 1, 1), "line")),
+        ((64, 16, 8), (8, 8, 8), ((8, 8, 8), "box")),
+        ((64, 16, 8), (4, 2, 2), ((4, 2, 2), "box")),
+        ((6, 5, 3), (8, 8, 8), ((6, 5, 3), "box")),
+        ((64, 16, 8), (8, 1, 1), ((8, 1, 1), "box")),
     ],
 )
 def test_block_shape_classification(dims, block, want):
     assert ps.block_shape_of(ps.PatchDims(*dims), block) == want
 
 
-@pytest.mark.parametrize("block", [(8, 8, 8), (32, 1, 1), (64, 2, 1), (64, 8, 2)])
-def test_non_line_plane_blocks_are_rejected(block):
+@pytest.mark.parametrize("block", [(16, 16, 16), (32, 1, 1), (64, 2, 1), (64, 8, 2), (9, 2, 2)])
+def test_unsupported_blocks_are_rejected(block):
     with pytest.raises(ValueError):
         ps.block_shape_of(ps.PatchDims(64, 16, 8), block)
 

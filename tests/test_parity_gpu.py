@@ -344,5 +344,5 @@ def test_singular_and_unsupported_inputs_raise():
         ps.InverseCache().get(ps.Stencil7(faces=(-1.0, -0.5, -1.0, -1.0, -1.0, -1.0)), (8, 8, 1))
     lv = _two_patch(3)
     with pytest.raises(ValueError):
-        ps.smooth(lv, ps.SmootherConfig(scheme="block_jacobi", block_dims=(8, 8, 8)), ps.InverseCache())
+        ps.smooth(lv, ps.SmootherConfig(scheme="block_jacobi", block_dims=(16, 16, 16)), ps.InverseCache())
     assert math.isfinite(ps.residual_norm(lv, ps.Stencil7()))

@@ -81,6 +81,10 @@ CONFIGS = {
                build=lambda: build_lattice((4, 4, 4), (128, 128, 128)),
                runs=[("chaotic_block_gs", "line", "wavefront"), ("chaotic_block_gs", "line", "chaotic"),
                      ("chaotic_block_gs", "plane", "wavefront"), ("block_jacobi", "line", None)]),
+    "F1": dict(desc="SURVEY f1: 512^3 single patch, box (cubic) blocks of the paper's Algorithm 2",
+               build=lambda: ps.build_level([(512, 512, 512)]),
+               runs=[("block_jacobi", (8, 8, 8), None), ("block_jacobi", (4, 4, 4), None),
+                     ("block_jacobi", (2, 2, 2), None), ("chaotic_block_gs", (8, 8, 8), "wavefront")]),
     "C5": dict(desc="1024^3 uniform grid, line Jacobi, 1 GPU",
                build=lambda: ps.build_level([(1024, 1024, 1024)]), runs=[("block_jacobi", "line", None)]),
 }
@@ -104,7 +108,10 @@ def main():
         for ri, (scheme, kind, mode) in enumerate(C["runs"]):
             if ri not in sel:
                 continue
-            bd = (p0.nx, 1, 1) if kind == "line" else (p0.nx, p0.ny, 1)
+            if isinstance(kind, tuple):  # box blocks
+                bd, kind = kind, "box" + "x".join(str(b) for b in kind)
+            else:
+                bd = (p0.nx, 1, 1) if kind == "line" else (p0.nx, p0.ny, 1)
             solver = "dst" if mode == "dst" else "auto"
             gs_mode = mode if mode in ("wavefront", "chaotic") else "wavefront"
             strat = ps.ExecutionStrategy.device(gs_mode=gs_mode)
