@@ -53,6 +53,10 @@ __device__ __forceinline__ void box_cp8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void box_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void box_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void box_wait() {
@@ -207,7 +211,7 @@ __device__ __forceinline__ void box_afrag(const double* __restrict__ T, int lane
 }
 template <int BX, int BY, int BZ>
 __device__ __forceinline__ void box_pass_mma(double* wc, int axis, const double (&a)[2], int lane, int warp,
-                                             const double* __restrict__ IL) {
+                                             const double* sc /* 4 per lane or null */) {
 #pragma unroll
   for (int tt = 0; tt < 2; ++tt) {
     const int t = warp * 2 + tt;
@@ -216,9 +220,9 @@ __device__ __forceinline__ void box_pass_mma(double* wc, int axis, const double 
     for (int ks = 0; ks < 2; ++ks)
       box_dmma(d0, d1, a[ks], wc[box_addr(axis, 8 * t + (lane >> 2), 4 * ks + (lane & 3))]);
     const int p = lane >> 2, n0 = 8 * t + 2 * (lane & 3);
-    if (IL) {  // forward z pass: scale by 1/lambda (p = k, line n = (i, j))
-      d0 *= box_ilam(IL, BX, BY, BZ, (n0 & 7) % BX, (n0 >> 3) % BY, p % BZ);
-      d1 *= box_ilam(IL, BX, BY, BZ, ((n0 + 1) & 7) % BX, ((n0 + 1) >> 3) % BY, p % BZ);
+    if (sc) {  // forward z pass: scale by 1/lambda (p = k, line n = (i, j))
+      d0 *= sc[2 * tt];
+      d1 *= sc[2 * tt + 1];
     }
     __syncwarp();
     wc[box_addr(axis, n0, p)] = d0;
@@ -231,7 +235,7 @@ __device__ __forceinline__ void box_pass_mma(double* wc, int axis, const double 
 // that dominated the generic kernel's instruction count (ncu: 28% IMAD plus
 // software division).  Regions are clipped at patch edges at run time.
 template <int BX, int BY, int BZ, int MX, int MY, int MZ>
-__global__ void __launch_bounds__(kBoxT) box_sweep_t(const PatchDev* __restrict__ patches,
+__global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restrict__ patches,
                                                      const unsigned char* __restrict__ active, StencilDev st,
                                                      double omega, const int4* __restrict__ blocks, int nblocks,
                                                      int inplace) {
@@ -240,8 +244,8 @@ __global__ void __launch_bounds__(kBoxT) box_sweep_t(const PatchDev* __restrict_
   constexpr int NC = RX * RY * RZ;
   // double-buffered staging: the next region's u halo and f stream in with
   // cp.async while this region computes (the sweep is otherwise latency-bound)
-  __shared__ double hbuf[2][kHp * kHs];
-  __shared__ double fbuf[2][NC];
+  __shared__ __align__(16) double hbuf[2][kHp * kHs];
+  __shared__ __align__(16) double fbuf[2][NC];
   __shared__ double wc[kBoxMax * kRp];
   const int tid = threadIdx.x;
   auto stage = [&](int b, int slot) {
@@ -253,21 +257,42 @@ __global__ void __launch_bounds__(kBoxT) box_sweep_t(const PatchDev* __restrict_
       const int rx = min(RX, nx - x0), ry = min(RY, ny - y0), rz = min(RZ, nz - z0);
       const long long px = nx + 2, pxy = px * (ny + 2);
       const double* ub = P.buf[active[B.x]] + (long long)z0 * pxy + (long long)y0 * px + x0;
-      for (int q = tid; q < HN; q += kBoxT) {
-        const int c = q / (HX * HY), r = q - c * (HX * HY), bb = r / HX, a = r - bb * HX;
-        if (a < rx + 2 && bb < ry + 2 && c < rz + 2)
-          box_cp8(&hbuf[slot][c * kHp + bb * kHs + a], ub + (long long)c * pxy + (long long)bb * px + a);
-      }
-      for (int q = tid; q < NC; q += kBoxT) {
-        const int k = q / (RX * RY), r = q - k * (RX * RY), j = r / RX, i = r - j * RX;
-        if (i < rx && j < ry && k < rz)
-          box_cp8(&fbuf[slot][q], P.f + ((long long)(z0 + k) * ny + (y0 + j)) * nx + x0 + i);
+      const double* fb0 = P.f + ((long long)z0 * ny + y0) * nx + x0;
+      // 16-byte copies when every row start is 16-byte aligned (full rows of an
+      // even-width patch at an even x0; the halo row stride kHs is even)
+      const bool wide = (RX % 2 == 0) && rx == RX && ((nx | x0) & 1) == 0 &&
+                        ((((uintptr_t)ub) | ((uintptr_t)fb0)) & 15) == 0;
+      if (wide) {
+        constexpr int HW = HX / 2, FW = RX / 2;  // 16-byte chunks per halo / f row
+        for (int q = tid; q < HW * HY * (RZ + 2); q += kBoxT) {
+          const int c = q / (HW * HY), r = q - c * (HW * HY), bb = r / HW, a = r - bb * HW;
+          if (bb < ry + 2 && c < rz + 2)
+            box_cp16(&hbuf[slot][c * kHp + bb * kHs + 2 * a], ub + (long long)c * pxy + (long long)bb * px + 2 * a);
+        }
+        for (int q = tid; q < FW * RY * RZ; q += kBoxT) {
+          const int k = q / (FW * RY), r = q - k * (FW * RY), j = r / FW, a = r - j * FW;
+          if (j < ry && k < rz)
+            box_cp16(&fbuf[slot][(k * RY + j) * RX + 2 * a], fb0 + ((long long)k * ny + j) * nx + 2 * a);
+        }
+      } else {
+        for (int q = tid; q < HN; q += kBoxT) {
+          const int c = q / (HX * HY), r = q - c * (HX * HY), bb = r / HX, a = r - bb * HX;
+          if (a < rx + 2 && bb < ry + 2 && c < rz + 2)
+            box_cp8(&hbuf[slot][c * kHp + bb * kHs + a], ub + (long long)c * pxy + (long long)bb * px + a);
+        }
+        for (int q = tid; q < NC; q += kBoxT) {
+          const int k = q / (RX * RY), r = q - k * (RX * RY), j = r / RX, i = r - j * RX;
+          if (i < rx && j < ry && k < rz)
+            box_cp8(&fbuf[slot][q], fb0 + ((long long)k * ny + j) * nx + i);
+        }
       }
     }
     box_commit();
   };
   stage(blockIdx.x, 0);
   int slot = 0;
+  const BoxFac* afF = nullptr;  // factor object whose fragments af/scl hold
+  double af[6][2], scl[4];
   for (int b = blockIdx.x; b < nblocks; b += gridDim.x, slot ^= 1) {
     stage(b + gridDim.x, slot ^ 1);
     box_wait<1>();
@@ -298,24 +323,33 @@ __global__ void __launch_bounds__(kBoxT) box_sweep_t(const PatchDev* __restrict_
     if constexpr (MX * BX == 8 && MY * BY == 8 && MZ * BZ == 8) {
       if (rx == 8 && ry == 8 && rz == 8) {  // interior region: tensor-core passes
         const int lane = tid & 31, warp = tid >> 5;
-        double a[2];
-        box_afrag<BX>(box_mat(F->F, 0, BX), lane, a);
-        box_pass_mma<BX, BY, BZ>(wc, 0, a, lane, warp, nullptr);
+        if (F != afF) {  // A fragments of the six transforms and this lane's 1/lambda, per factor object
+          afF = F;
+          box_afrag<BX>(box_mat(F->F, 0, BX), lane, af[0]);
+          box_afrag<BY>(box_mat(F->F, 1, BY), lane, af[1]);
+          box_afrag<BZ>(box_mat(F->F, 2, BZ), lane, af[2]);
+          box_afrag<BZ>(box_mat(F->B, 2, BZ), lane, af[3]);
+          box_afrag<BY>(box_mat(F->B, 1, BY), lane, af[4]);
+          box_afrag<BX>(box_mat(F->B, 0, BX), lane, af[5]);
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt) {
+            const int n0 = 8 * (warp * 2 + tt) + 2 * (lane & 3), pz = lane >> 2;
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              scl[2 * tt + e] = box_ilam(F->IL, BX, BY, BZ, ((n0 + e) & 7) % BX, ((n0 + e) >> 3) % BY, pz % BZ);
+          }
+        }
+        box_pass_mma<BX, BY, BZ>(wc, 0, af[0], lane, warp, nullptr);
         __syncthreads();
-        box_afrag<BY>(box_mat(F->F, 1, BY), lane, a);
-        box_pass_mma<BX, BY, BZ>(wc, 1, a, lane, warp, nullptr);
+        box_pass_mma<BX, BY, BZ>(wc, 1, af[1], lane, warp, nullptr);
         __syncthreads();
-        box_afrag<BZ>(box_mat(F->F, 2, BZ), lane, a);
-        box_pass_mma<BX, BY, BZ>(wc, 2, a, lane, warp, F->IL);
+        box_pass_mma<BX, BY, BZ>(wc, 2, af[2], lane, warp, scl);
         __syncthreads();
-        box_afrag<BZ>(box_mat(F->B, 2, BZ), lane, a);
-        box_pass_mma<BX, BY, BZ>(wc, 2, a, lane, warp, nullptr);
+        box_pass_mma<BX, BY, BZ>(wc, 2, af[3], lane, warp, nullptr);
         __syncthreads();
-        box_afrag<BY>(box_mat(F->B, 1, BY), lane, a);
-        box_pass_mma<BX, BY, BZ>(wc, 1, a, lane, warp, nullptr);
+        box_pass_mma<BX, BY, BZ>(wc, 1, af[4], lane, warp, nullptr);
         __syncthreads();
-        box_afrag<BX>(box_mat(F->B, 0, BX), lane, a);
-        box_pass_mma<BX, BY, BZ>(wc, 0, a, lane, warp, nullptr);
+        box_pass_mma<BX, BY, BZ>(wc, 0, af[5], lane, warp, nullptr);
         __syncthreads();
 #pragma unroll
         for (int q0 = 0; q0 < 512; q0 += kBoxT) {  // relax, row-contiguous stores
