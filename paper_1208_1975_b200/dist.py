@@ -33,7 +33,8 @@ import torch.distributed as dist
 from . import _lib
 from .grid import Level, Patch, PatchDims, _int3
 
-__all__ = ["slab_range", "SlabDomain", "exchange_planes", "gather_plane_sums"]
+__all__ = ["slab_range", "SlabDomain", "exchange_planes", "gather_plane_sums", "PatchLevelDomain",
+           "dist_smooth", "dist_smooth_level"]
 
 
 def slab_range(nz, world, rank):
@@ -258,3 +259,162 @@ def jacobi_step_overlapped(domain, dp, omega, slot, events=None):
     dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
     domain.finish_exchange(reqs)
     domain.unpack(dp)
+
+
+# ---------------------------------------------------------------------------
+# Multi-patch levels across GPUs: patches are independent
+# within a step, so partition_patches (runtime.py:92-131) assigns them to
+# ranks; interface copies between patches of one rank run in the device
+# ghost refresh, copies between ranks are packed, sent, received and
+# unpacked after it (physical ghosts first, interfaces second, as
+# grid.py:507-517).
+# ---------------------------------------------------------------------------
+class _PatchSpec:
+    """A patch description without buffers (for the global adjacency)."""
+
+    def __init__(self, dims, origin):
+        self.dims = dims if isinstance(dims, PatchDims) else PatchDims(*_int3(dims, "dims"))
+        self.origin = _int3(origin, "origin")
+
+    @property
+    def global_box(self):
+        return tuple((o, o + n) for o, n in zip(self.origin, self.dims.shape))
+
+
+class _SpecLevel:
+    def __init__(self, specs):
+        self.patches = specs
+
+
+class PatchLevelDomain:
+    """This rank's share of a multi-patch level.
+
+    ``specs``: list of (dims, origin) for every patch of the global level, in
+    global order.  ``owner[g]`` is the rank of global patch g (greedy cell
+    balance by default); ``mine`` the global indices owned here, ascending;
+    ``level`` a Level of the owned patches with the interface copies among
+    them; ``sends`` / ``recvs`` the cross-rank copies touching this rank."""
+
+    def __init__(self, specs, rank, world, device=None, group=None, assignment="greedy"):
+        from .grid import _abutments
+        from .runtime import partition_patches
+
+        self.specs = [_PatchSpec(d, o) for d, o in specs]
+        self.rank, self.world, self.group = rank, world, group
+        self.adjacency = _abutments(self.specs)
+        buckets = partition_patches(_SpecLevel(self.specs), world, assignment)
+        self.owner = {g: r for r, b in enumerate(buckets) for g in b}
+        self.mine = sorted(g for g, r in self.owner.items() if r == rank)
+        if not self.mine:
+            raise ValueError(f"rank {rank} owns no patch ({len(self.specs)} patches over {world} ranks)")
+        local = {g: i for i, g in enumerate(self.mine)}
+        self.local_index = local
+        self.patches = [Patch(self.specs[g].dims, self.specs[g].origin, device=device) for g in self.mine]
+        from .grid import InterfaceCopy
+
+        inner = [InterfaceCopy(local[c.src], local[c.dst], c.src_lo, c.dst_lo, c.extent)
+                 for c in self.adjacency if c.src in local and c.dst in local]
+        self.level = Level(self.patches, adjacency=inner)
+        # cross-rank copies, in global adjacency order (both sides agree)
+        self.sends = [c for c in self.adjacency if c.src in local and c.dst not in local]
+        self.recvs = [c for c in self.adjacency if c.dst in local and c.src not in local]
+
+    def _src_view(self, c):
+        p = self.patches[self.local_index[c.src]]
+        sl = tuple(slice(1 + lo, 1 + lo + e) for lo, e in zip(c.src_lo, c.extent))
+        return p.u[sl]
+
+    def _dst_view(self, c):
+        p = self.patches[self.local_index[c.dst]]
+        sl = tuple(slice(1 + lo, 1 + lo + e) for lo, e in zip(c.dst_lo, c.extent))
+        return p.u[sl]
+
+    def exchange(self):
+        """Cross-rank interface copies of the active buffers: pack the source
+        interior layers, send/receive (grouped), unpack into the ghosts."""
+        if self.world == 1:
+            return
+        out = [self._src_view(c).contiguous() for c in self.sends]
+        inb = [torch.empty(tuple(c.extent), dtype=torch.float64, device=self.patches[0].device) for c in self.recvs]
+        gloo = out and out[0].is_cuda and dist.get_backend(self.group) == "gloo" or (
+            inb and inb[0].is_cuda and dist.get_backend(self.group) == "gloo")
+        if gloo:  # host-staged (several ranks on one GPU)
+            out_h = [t.cpu() for t in out]
+            in_h = [torch.empty(t.shape, dtype=t.dtype) for t in inb]
+        else:
+            out_h, in_h = out, inb
+        ops = [dist.P2POp(dist.isend, t, self.owner[c.dst], self.group) for t, c in zip(out_h, self.sends)]
+        ops += [dist.P2POp(dist.irecv, t, self.owner[c.src], self.group) for t, c in zip(in_h, self.recvs)]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for c, t in zip(self.recvs, in_h):
+            self._dst_view(c).copy_(t)
+
+    def plane_slots(self):
+        """(global plane offset, nz) of every owned patch (global patch order)."""
+        off, acc = {}, 0
+        for g, s in enumerate(self.specs):
+            off[g] = acc
+            acc += s.dims.nz
+        return [(off[g], self.specs[g].dims.nz) for g in self.mine], acc
+
+
+def dist_smooth_level(domain, config, cache):
+    """``smooth`` on a multi-patch level split over ranks by patch: every rank
+    calls it with its own ``PatchLevelDomain``; returns the global history on
+    every rank (bit-identical to the single-process run: per-plane partial
+    sums are reduced in global plane order by the same fixed tree)."""
+    from .smoother import _Plan, _gs_mode
+
+    level = domain.level
+    plan = _Plan(level, config, cache)
+    dp = plan.dev
+    lib = _lib.load()
+    steps = config.steps
+    jac = config.scheme == "block_jacobi"
+    with torch.cuda.device(plan.device):
+        dp.reserve(steps + 1)
+        dp.refresh(_lib.GHOST_ALL)
+        domain.exchange()
+        if not jac:
+            dp.residual(0)
+        mode = _gs_mode(config)
+        for s in range(steps):
+            if jac:
+                dp.jacobi(config.omega, s)
+                for p in level.patches:
+                    p.swap_buffers()
+                dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+            else:
+                dp.gs(config.omega, mode)
+                dp.refresh(_lib.GHOST_ALL)
+            domain.exchange()
+            if not jac:
+                dp.residual(s + 1)
+        if jac:
+            dp.residual(steps)
+        slots, total = domain.plane_slots()
+        nloc = sum(n for _, n in slots)
+        local = torch.empty((steps + 1, nloc), dtype=torch.float64, device=plan.device)
+        for s in range(steps + 1):
+            dp.plane_sums(s, local[s])
+        full = torch.zeros((steps + 1, total), dtype=torch.float64, device=plan.device)
+        c = 0
+        for off, n in slots:
+            full[:, off:off + n] = local[:, c:c + n]
+            c += n
+        if domain.world > 1:  # each plane has exactly one owner: the sum is exact
+            if full.is_cuda and dist.get_backend(domain.group) == "gloo":
+                fh = full.cpu()
+                dist.all_reduce(fh, group=domain.group)
+                full.copy_(fh)
+            else:
+                dist.all_reduce(full, group=domain.group)
+        out = torch.empty(steps + 1, dtype=torch.float64, device=plan.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(plan.device).cuda_stream)
+        for s in range(steps + 1):
+            row = full[s].contiguous()
+            _lib.check(lib.psm_tree_sum(ctypes.c_void_p(row.data_ptr()), row.numel(),
+                                        ctypes.c_void_p(out[s:].data_ptr()), stream), "tree_sum")
+        return [math.sqrt(v) for v in out.cpu().tolist()]

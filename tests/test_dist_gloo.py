@@ -121,3 +121,54 @@ def test_slab_ranges_tile_the_grid(nz, world):
     assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
     sizes = [b - a for a, b in spans]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _level_main(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1208_1975_b200.dist import PatchLevelDomain
+
+        specs = [((4, 3, 2), (a * 4, b * 3, c * 2)) for c in range(2) for b in range(2) for a in range(3)]
+        dom = PatchLevelDomain(specs, rank, world, device="cpu")
+        for g, p in zip(dom.mine, dom.patches):
+            p.u[...] = -1.0
+            p.interior[...] = torch.arange(24, dtype=torch.float64).reshape(4, 3, 2) + 100.0 * g
+        dom.exchange()
+        for g, p in zip(dom.mine, dom.patches):
+            np.save(os.path.join(out_dir, f"u{g}.npy"), p.u.numpy())
+        np.save(os.path.join(out_dir, f"owner{rank}.npy"), np.array(dom.mine))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_patch_partition_exchange_fills_cross_rank_ghosts(tmp_path):
+    """PatchLevelDomain: greedy patch-to-rank map, and exchange() writes every
+    cross-rank ghost layer with the neighbour's interior layer (what the
+    device refresh does for same-rank pairs)."""
+    from paper_1208_1975_b200.dist import PatchLevelDomain, _PatchSpec
+    from paper_1208_1975_b200.grid import _abutments
+
+    world = 3
+    mp.spawn(_level_main, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    owned = sorted(int(g) for r in range(world) for g in np.load(tmp_path / f"owner{r}.npy"))
+    assert owned == list(range(12))
+    specs = [((4, 3, 2), (a * 4, b * 3, c * 2)) for c in range(2) for b in range(2) for a in range(3)]
+    owner = {}
+    for r in range(world):
+        for g in np.load(tmp_path / f"owner{r}.npy"):
+            owner[int(g)] = r
+    adj = _abutments([_PatchSpec(d, o) for d, o in specs])
+    checked = 0
+    for c in adj:
+        if owner[c.src] == owner[c.dst]:
+            continue
+        src = np.load(tmp_path / f"u{c.src}.npy")
+        dst = np.load(tmp_path / f"u{c.dst}.npy")
+        s = tuple(slice(1 + lo, 1 + lo + e) for lo, e in zip(c.src_lo, c.extent))
+        d = tuple(slice(1 + lo, 1 + lo + e) for lo, e in zip(c.dst_lo, c.extent))
+        np.testing.assert_array_equal(dst[d], src[s])
+        checked += 1
+    assert checked > 0
