@@ -617,8 +617,22 @@ static int zmarch_units(psm_plan* P, int p0, int p1, int ka, int kb, void** d_un
   long long cols = 0;
   for (int p = p0; p < p1; ++p) cols += P->hp[p].tpp;
   const long long planes = std::max(1, (kb < 0 ? P->hp[p0].nz : kb) - ka);
-  const long long target = 8LL * 148;
-  int kc = (int)std::min<long long>(128, std::max<long long>(4, cols * planes / target));
+  // plane-chunk length: minimise the busiest persistent CTA's work,
+  // ceil(units / SMs) * (chunk + ~2 planes of halo and pipeline fill)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int kc = (int)planes;
+  double best = 1e300;
+  for (long long nch = 1; nch <= std::min<long long>(planes, 256); ++nch) {
+    const long long len = (planes + nch - 1) / nch;
+    if (len < 4 && nch > 1) break;
+    const double cost = (double)((cols * nch + sms - 1) / sms) * (double)(len + 2);
+    if (cost < best - 1e-9) {
+      best = cost;
+      kc = (int)len;
+    }
+  }
   std::vector<int> u;
   for (int p = p0; p < p1; ++p) {
     const PatchDev& h = P->hp[p];
