@@ -51,6 +51,7 @@ constexpr int kGsPub = 4;     // wavefront mode: rows per release of the cross-C
 // uniform chunk-interior tables (passed by value: constant-bank operands)
 struct GsUniform {
   double invm[8], loinv[8], cp[8], g[8], h[8];
+  double tinv[8][8];  // explicit inverse of the chunk interior block (row i: y_i = sum_p tinv[i][p] r_p)
   int npcr;  // PCR steps until the remaining interface couplings are < 1e-20 (<= 5: exact)
 };
 
@@ -295,11 +296,9 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
 #endif
       for (int j = 0; j < ny; ++j) {
         GS_PROF(0, 0.0);
-        issue(j + P);
-        GS_PROF(1, 0.0);
-        cp_wait<P>();
+        cp_wait<P - 1>();  // G(j) landed (G(j+1..j+P-1) may still fly)
         __syncwarp();
-        GS_PROF(2, 0.0);
+        GS_PROF(1, 0.0);
         const int s = (j % D) * SLOT;
         double nxt[NC], zp[NC], fv[NC], zm[NC];
 #pragma unroll
@@ -309,6 +308,33 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           fv[i] = Fr[s + i * IS + lane];
         }
         const double gl = Ur[s + NC * IS], gr = Ur[s + NC * IS + 1];
+        GS_PROF(2, 0.0);
+        // ---- residual prefix, reference order (stencil.py:106-111): c u,
+        // -x, +x, -y, +y need nothing from plane k-1, so they run before the
+        // hand-off wait; -z (new) and +z follow it
+        double acc[NC];
+        {
+          const double lft = __shfl_up_sync(0xffffffffu, cen[NC - 1], 1);
+          const double rgt = __shfl_down_sync(0xffffffffu, cen[0], 1);
+#pragma unroll
+          for (int i = 0; i < NC; ++i) {
+            const double xl = i > 0 ? cen[i > 0 ? i - 1 : 0] : (lane == 0 ? gl : lft);
+            const double xr = i < NC - 1 ? cen[i < NC - 1 ? i + 1 : 0] : (lane == 31 ? gr : rgt);
+            if (UNIT) {  // faces all -1: face*nbr is exactly -nbr, same roundings
+              double a = __dmul_rn(st.c, cen[i]);
+              a = __dsub_rn(a, xl);
+              a = __dsub_rn(a, xr);
+              a = __dsub_rn(a, ym[i]);
+              acc[i] = __dsub_rn(a, nxt[i]);
+            } else {
+              double a = __dmul_rn(st.c, cen[i]);
+              a = __dadd_rn(a, __dmul_rn(st.xm, xl));
+              a = __dadd_rn(a, __dmul_rn(st.xp, xr));
+              a = __dadd_rn(a, __dmul_rn(st.ym, ym[i]));
+              acc[i] = __dadd_rn(a, __dmul_rn(st.yp, nxt[i]));
+            }
+          }
+        }
         // ---- u(j, k-1), new ----------------------------------------------
         if (warp > 0) {
           const int hs = j % DH;
@@ -346,37 +372,28 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           for (int i = 0; i < NC; ++i) zm[i] = mrow[i];
         }
         GS_PROF(3, zm[NC - 1] + fv[NC - 1] + nxt[NC - 1] + zp[NC - 1]);
-        // ---- residual in the reference operation order ------------------
         double r[NC];
-        {
-          const double lft = __shfl_up_sync(0xffffffffu, cen[NC - 1], 1);
-          const double rgt = __shfl_down_sync(0xffffffffu, cen[0], 1);
 #pragma unroll
-          for (int i = 0; i < NC; ++i) {
-            const double xl = i > 0 ? cen[i > 0 ? i - 1 : 0] : (lane == 0 ? gl : lft);
-            const double xr = i < NC - 1 ? cen[i < NC - 1 ? i + 1 : 0] : (lane == 31 ? gr : rgt);
-            if (UNIT) {  // faces all -1: face*nbr is exactly -nbr, same roundings
-              double acc = __dmul_rn(st.c, cen[i]);
-              acc = __dsub_rn(acc, xl);
-              acc = __dsub_rn(acc, xr);
-              acc = __dsub_rn(acc, ym[i]);
-              acc = __dsub_rn(acc, nxt[i]);
-              acc = __dsub_rn(acc, zm[i]);
-              acc = __dsub_rn(acc, zp[i]);
-              r[i] = __dsub_rn(fv[i], acc);
-            } else {
-              r[i] = residual7(st, fv[i], cen[i], xl, xr, ym[i], nxt[i], zm[i], zp[i]);
-            }
+        for (int i = 0; i < NC; ++i) {
+          if (UNIT) {
+            r[i] = __dsub_rn(fv[i], __dsub_rn(__dsub_rn(acc[i], zm[i]), zp[i]));
+          } else {
+            const double a = __dadd_rn(acc[i], __dmul_rn(st.zm, zm[i]));
+            r[i] = __dsub_rn(fv[i], __dadd_rn(a, __dmul_rn(st.zp, zp[i])));
           }
         }
         GS_PROF(4, r[NC - 1] + r[0]);
         // ---- exact line solve: local elimination + PCR ------------------
+        // chunk interior: y = T_int^{-1} r as independent dot products (depth
+        // M instead of the 2M-1 dependent steps of Thomas)
         double y[NC];
 #pragma unroll
-        for (int i = 0; i < M; ++i)
-          y[i] = i == 0 ? r[0] * T.invm[0] : fma(-T.loinv[i], y[i > 0 ? i - 1 : 0], r[i] * T.invm[i]);
+        for (int i = 0; i < M; ++i) {
+          double a = 0.0;
 #pragma unroll
-        for (int i = M - 2; i >= 0; --i) y[i] = fma(-T.cp[i], y[i + 1], y[i]);
+          for (int p = 0; p < M; ++p) a = fma(T.tinv[i][p], r[p], a);
+          y[i] = a;
+        }
         GS_PROF(5, y[0] + y[M > 0 ? M - 1 : 0]);
         double rho = q[0] * r[NC - 1];
         if (M > 0) {
@@ -424,6 +441,7 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
 #pragma unroll
           for (int i = 0; i < NC; ++i) __stcg(dst + i * 32 + lane, h[dpos[i]]);
         }
+        issue(j + P);  // prefetch, off the hand-off critical path
         GS_PROF(8, 0.0);
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
@@ -532,6 +550,12 @@ static int gs_pipe_tables(int nc, long double lo, long double d, long double up,
     e[0] = 0;
     e[m - 1] = up;
     solve(e, h);
+  }
+  for (int c = 0; c < m; ++c) {  // columns of the interior inverse
+    long double e[8] = {0}, col[8];
+    e[c] = 1.0L;
+    solve(e, col);
+    for (int i = 0; i < m; ++i) T.tinv[i][c] = (double)col[i];
   }
   for (int i = 0; i < m; ++i) {
     T.invm[i] = (double)invm[i];
