@@ -179,8 +179,44 @@ def box_cases(ps):
     random_patch_case(ps, "box_gs_9x9x9_b3x3x3", (9, 9, 9), (3, 3, 3), "chaotic_block_gs", 3, seed=27)
 
 
+CLI_CASES = {
+    "cli_converge_default_12": ["converge", "--patch-size", "12x12x12", "--steps", "4"],
+    "cli_converge_gs_10x9x8": ["converge", "--patch-size", "10x9x8", "--scheme", "chaotic-gs", "--steps", "3",
+                               "--block-size", "4x4x2"],
+    "cli_smooth_box_16_n2": ["smooth", "--patch-size", "16x16x16", "--num-patches", "2", "--steps", "3"],
+    "cli_smooth_lines_mixed": ["smooth", "--patch-size", "24x8x8", "--patch-size", "16x8x8", "--block-size",
+                               "24x1x1", "--scheme", "chaotic-gs", "--steps", "2"],
+    "cli_smooth_plane_w06": ["smooth", "--patch-size", "16x12x6", "--block-size", "16x12x1", "--omega", "0.6",
+                             "--steps", "3"],
+}
+
+
+def cli_cases():
+    """The reference CLI's own CSV output (cli.py:319-358) for small cases."""
+    sys.path.insert(0, REF)
+    import io
+    from contextlib import redirect_stdout
+
+    from patchsmooth import cli
+
+    for name, argv in CLI_CASES.items():
+        buf = io.StringIO()
+        with redirect_stdout(buf):
+            rc = cli.main(argv)
+        assert rc == 0, (name, rc)
+        path = os.path.join(OUT, name + ".csv")
+        with open(path, "w", newline="") as fh:
+            fh.write(buf.getvalue())
+        with open(path + ".args", "w") as fh:
+            fh.write(" ".join(argv) + "\n")
+        print(f"wrote {name}: {os.path.getsize(path)} bytes")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--only-cli" in sys.argv:
+        cli_cases()
+        return
     if "--only-box" in sys.argv:
         box_cases(_ref())
         return
@@ -213,6 +249,7 @@ def main():
         zsplit_case(ps, f"zsplit_line_{tag}_32x8x8_in4", (32, 8, 8), 4, (32, 1, 1), scheme, 3)
     zsplit_case(ps, "zsplit_plane_jac_8x8x8_in2", (8, 8, 8), 2, (8, 8, 1), "block_jacobi", 2)
     box_cases(ps)
+    cli_cases()
     host_logic_case(ps)
     # the CLI's own inputs (seed 42, f = 0) -- SURVEY section 8c golden histories
     seeded_case(ps, "seeded_line_jac_64", (64, 64, 64), (64, 1, 1), "block_jacobi", 10, (0, 31, 63))

@@ -24,7 +24,8 @@ from . import _lib
 from .grid import _int3, default_device
 from .stencil import Stencil7
 
-__all__ = ["SingularMatrixError", "BlockFactors", "InverseCache", "block_kind", "plane_solver"]
+__all__ = ["SingularMatrixError", "BlockFactors", "InverseCache", "block_kind", "plane_solver",
+           "multiply_back_error"]
 
 _MAX_DENSE = 8192
 
@@ -39,6 +40,15 @@ def plane_solver(mode=None):
         raise ValueError(f"plane solver must be 'auto' or 'dst', got {mode!r}")
     prev = _lib.load().psm_plane_solver(modes[mode] if mode is not None else -1)
     return "dst" if prev == _lib.PLANE_DST else "auto"
+
+
+def multiply_back_error(a, ainv):
+    """||A Ainv - I||_inf (blocklinalg.py:108-113), on the tensors' device."""
+    a = torch.as_tensor(a, dtype=torch.float64)
+    ainv = torch.as_tensor(ainv, dtype=torch.float64, device=a.device)
+    resid = a @ ainv
+    resid.diagonal().sub_(1.0)
+    return float(resid.abs().sum(dim=1).max())
 
 
 class SingularMatrixError(ValueError):

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 
 from . import _lib
 
-__all__ = ["Stencil7", "FACE_OFFSETS"]
+__all__ = ["Stencil7", "FACE_OFFSETS", "assemble_block_matrix"]
 
 # stencil.py:42-49
 FACE_OFFSETS = ((-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1))
@@ -44,3 +44,28 @@ class Stencil7:
         for i, c in enumerate(self.faces):
             s.faces[i] = c
         return s
+
+
+def assemble_block_matrix(stencil, extent, device=None):
+    """Dense operator of one block, couplings inside the block only
+    (stencil.py:115-138), cells x fastest, as a float64 tensor on ``device``
+    (for the ``inverses`` report and multiply-back checks; the smoother never
+    forms it)."""
+    import torch
+
+    from .grid import _int3, default_device
+
+    ex, ey, ez = _int3(extent, "extent")
+    if min(ex, ey, ez) < 1:
+        raise ValueError(f"extent must be positive, got {(ex, ey, ez)}")
+    dev = torch.device(device) if device is not None else default_device()
+    n = ex * ey * ez
+    a = torch.zeros((n, n), dtype=torch.float64, device=dev)
+    idx = torch.arange(n, device=dev)
+    x, y, z = idx % ex, (idx // ex) % ey, idx // (ex * ey)
+    a[idx, idx] = stencil.center
+    for c, (dx, dy, dz) in zip(stencil.faces, FACE_OFFSETS):
+        px, py, pz = x + dx, y + dy, z + dz
+        ok = (px >= 0) & (px < ex) & (py >= 0) & (py < ey) & (pz >= 0) & (pz < ez)
+        a[idx[ok], (px + ex * (py + ey * pz))[ok]] = c
+    return a
