@@ -9,7 +9,8 @@ timeout -s KILL 600 python tools/bench_configs.py > $O/configs.jsonl 2>&1; echo 
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv \
   python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
 python tools/launch_summary.py $O/launches_bench.csv > $O/launches_bench.txt 2>&1
-for c in C2 C3 C4; do
+timeout -s KILL 300 python __graft_entry__.py > $O/smoke.log 2>&1; echo "smoke rc=$?"
+for c in C2 C3 C4 F1; do
   timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$c.csv \
     python tools/bench_configs.py --only $c --steps 1 --warmup 1 > /dev/null 2>&1
   python tools/launch_summary.py $O/launches_$c.csv > $O/launches_$c.txt 2>&1
@@ -21,7 +22,9 @@ sweep_ms((256, 256, 256), reps=1)
 PY
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:line_gs_pipe -s 2 -c 1 -o $O/gs_pipe_256 python /tmp/one_gs.py > /dev/null 2>&1; echo "ncu gs rc=$?"
 bash tools/ncu_plane.sh 512 round/plane_band_512 > /dev/null 2>&1; echo "ncu band rc=$?"
-for r in gs_pipe_256 plane_band_512; do
+bash tools/ncu_box.sh 512 8 round/box_8_512 > /dev/null 2>&1; echo "ncu box rc=$?"
+bash tools/ncu_line.sh 1024 round/line_jacobi_1024 > /dev/null 2>&1; echo "ncu line rc=$?"
+for r in gs_pipe_256 plane_band_512 box_8_512 line_jacobi_1024; do
   python tools/ncu_summary.py $O/$r.ncu-rep > $O/${r}_summary.txt 2>&1
 done
 echo done
