@@ -77,9 +77,11 @@ class BlockFactors:
     ``block_kind``) is built eagerly; a plan may also ask for the box form of
     a line or plane extent (the same inverse, applied by the box kernel)."""
 
-    def __init__(self, stencil, extent, device):
+    def __init__(self, stencil, extent, device, kind=None):
         self.extent = _int3(extent, "extent")
-        self.kind = block_kind(self.extent)
+        self.kind = kind if kind is not None else block_kind(self.extent)
+        if self.kind not in ("line", "plane", "box"):
+            raise ValueError(f"unknown block form {self.kind!r}")
         self.stencil = stencil
         self.device = torch.device(device)
         if self.device.type != "cuda":
@@ -158,8 +160,10 @@ class InverseCache:
         self._stencil = None
         self._inversions = 0
 
-    def get(self, stencil, extent, device=None):
-        """The factor object for ``extent``, built on first use."""
+    def get(self, stencil, extent, device=None, kind=None):
+        """The factor object for ``extent``, built on first use; ``kind``
+        ('line' | 'plane' | 'box') names the device form the caller needs
+        first (default: the extent's natural form, ``block_kind``)."""
         if not isinstance(stencil, Stencil7):
             raise TypeError("stencil must be a Stencil7")
         extent = _int3(extent, "extent")
@@ -177,7 +181,7 @@ class InverseCache:
                 raise ValueError("cache already bound to a different stencil")
             entry = self._entries.get(key)
             if entry is None:
-                entry = BlockFactors(stencil, extent, dev)
+                entry = BlockFactors(stencil, extent, dev, kind)
                 self._inversions += 1
                 self._entries[key] = entry
             return entry

@@ -116,7 +116,7 @@ class _Plan:
         for p in level.patches:
             ext, kind = block_shape_of(p.dims, config.block_dims)
             kinds.add(kind)
-            factors.append(cache.get(config.stencil, ext, dev))
+            factors.append(cache.get(config.stencil, ext, dev, kind))
         if len(kinds) != 1:
             raise ValueError(f"block_dims {config.block_dims} make mixed line/plane/box blocks on this level")
         self.kind = kinds.pop()
