@@ -46,8 +46,14 @@ constexpr int kBoxMax = 8;     // largest extent per axis
 constexpr int kBoxT = 128;     // threads per block CTA
 constexpr int kHs = 10;        // halo box row stride (ex + 2 <= 10)
 constexpr int kHp = 100;       // halo box plane stride
-constexpr int kRs = 9;         // work cube row stride (odd: conflict-free rows)
-constexpr int kRp = 8 * 9;     // work cube plane stride
+#ifndef PSM_BOX_RS
+#define PSM_BOX_RS 12
+#define PSM_BOX_RP 100
+#endif
+// work cube strides: rows 12, planes 100 (both = 4 mod 8 doubles) make the
+// DMMA B-fragment loads of all three axes bank-conflict free
+constexpr int kRs = PSM_BOX_RS;
+constexpr int kRp = PSM_BOX_RP;
 
 __device__ __forceinline__ void box_cp8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
