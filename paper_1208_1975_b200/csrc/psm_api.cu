@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <map>
@@ -37,6 +38,8 @@ cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char
 cudaError_t launch_plane_sums(const PatchDev* patches, int npatch, const double* partials, double* plane_sums,
                               int nplanes, cudaStream_t stream);
 cudaError_t launch_tree_sum(const double* in, long long n, double* out, cudaStream_t stream);
+cudaError_t launch_history_reduce(const PatchDev* patches, int npatch, const double* partials, long long tstride,
+                                  int nplanes, int nslots, double* out, cudaStream_t stream);
 cudaError_t launch_halo_unpack(double* dst_plane, const double* src_plane, int px, int py, cudaStream_t stream);
 cudaError_t launch_line_gs(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, int* flags, long long nunits,
@@ -666,7 +669,28 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
     const int nx = P->hp[p].nx;
     int q = p + 1;
     while (q < pb && P->hp[q].nx == nx) ++q;
-    if (P->tiled && line_nx_specialised(nx) && P->hp[p].R == zmarch_rows(nx)) {
+    long long gcells = 0;  // cells of this group's plane range
+    for (int r = p; r < q; ++r)
+      gcells += (long long)P->hp[r].nx * P->hp[r].ny * ((kb < 0 ? P->hp[r].nz : kb) - ka);
+    static const long long zmin = [] {
+      const char* e = getenv("PSM_ZMARCH_MIN_CELLS");
+      return e ? atoll(e) : (1LL << 21);
+    }();
+    if (P->tiled && line_nx_specialised(nx) && gcells < zmin) {
+      // small groups: the one-tile-per-CTA specialised kernel (no TMA ring to
+      // fill, no persistent pipeline to drain) is latency-cheaper
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      for (int r = p; r < q; ++r) {
+        const PatchDev& h = P->hp[r];
+        const int a = ka, b = (kb < 0) ? h.nz : kb;
+        const long long t0 = h.tile0 + (long long)a * h.tpp, t1 = h.tile0 + (long long)b * h.tpp;
+        CUDA_TRY(launch_line_nx(nx, unit ? 1 : 0, P->d_patches, P->npatch, da, P->st, omega, part, t0, t1,
+                                line_nx_occupancy(nx) * sms, s));
+        P->launches += 1;
+      }
+    } else if (P->tiled && line_nx_specialised(nx) && P->hp[p].R == zmarch_rows(nx)) {
       void* units;
       int nu;
       int rc = zmarch_units(P, p, q, ka, kb, &units, &nu);
@@ -987,11 +1011,10 @@ int psm_history_sumsq(psm_plan* P, int nslots, double* out_host, void* stream) {
   if (nslots > P->cap_slots) return fail(PSM_EINVAL, "only %d history slots reserved", P->cap_slots);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t tstride = std::max<long long>(1, P->ntiles);
-  for (int k = 0; k < nslots; ++k) {
-    double* ps = P->d_plane_sums + (size_t)k * std::max(1, P->nplanes);
-    CUDA_TRY(launch_plane_sums(P->d_patches, P->npatch, P->d_partials + k * tstride, ps, P->nplanes, s));
-    CUDA_TRY(launch_tree_sum(ps, P->nplanes, P->d_sums + k, s));
-    P->launches += 2;
+  if (nslots > 0) {  // one launch for every slot (same bits as plane sums + tree per slot)
+    CUDA_TRY(launch_history_reduce(P->d_patches, P->npatch, P->d_partials, (long long)tstride, P->nplanes, nslots,
+                                   P->d_sums, s));
+    P->launches += 1;
   }
   if (nslots > 0) {
     CUDA_TRY(cudaMemcpyAsync(out_host, P->d_sums, nslots * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -163,6 +163,47 @@ cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char
   return cudaGetLastError();
 }
 
+// All history slots at once: block s reduces slot s with exactly the
+// arithmetic of plane_sums_kernel followed by tree_sum_kernel (each thread
+// sums its chunk of planes in order, every plane's tiles in order, then the
+// same pairwise tree), so the bits equal the two-launch path.
+__global__ void __launch_bounds__(1024) history_reduce_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                                              const double* __restrict__ partials, long long tstride,
+                                                              int nplanes, double* __restrict__ out) {
+  __shared__ double buf[1024];
+  const int t = threadIdx.x;
+  const double* part = partials + (long long)blockIdx.x * tstride;
+  const long long chunk = ((long long)nplanes + 1023) / 1024;
+  const long long b = t * chunk, e = min((long long)nplanes, b + chunk);
+  double s = 0.0;
+  for (long long gp = b; gp < e; ++gp) {
+    int lo = 0, hi = npatch - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (patches[mid].plane0 <= gp) lo = mid; else hi = mid - 1;
+    }
+    const PatchDev& P = patches[lo];
+    const double* src = part + P.tile0 + (gp - P.plane0) * (long long)P.tpp;
+    double ps = 0.0;
+    for (int q = 0; q < P.tpp; ++q) ps += src[q];
+    s += ps;
+  }
+  buf[t] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (t < w) buf[t] = buf[t] + buf[t + w];
+    __syncthreads();
+  }
+  if (t == 0) out[blockIdx.x] = buf[0];
+}
+
+cudaError_t launch_history_reduce(const PatchDev* patches, int npatch, const double* partials, long long tstride,
+                                  int nplanes, int nslots, double* out, cudaStream_t stream) {
+  if (nslots <= 0) return cudaSuccess;
+  history_reduce_kernel<<<nslots, 1024, 0, stream>>>(patches, npatch, partials, tstride, nplanes, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_plane_sums(const PatchDev* patches, int npatch, const double* partials, double* plane_sums,
                               int nplanes, cudaStream_t stream) {
   if (nplanes == 0) return cudaSuccess;
