@@ -7,8 +7,11 @@ omega 0.8), z-slab decomposed over N GPUs (one process per GPU, launched by
 torchrun for N > 1); strong scaling, the global grid is fixed.  A step is one
 smoother step as the reference runs it (smoother.py:138-153): the line-Jacobi
 sweep with its fused residual-norm partials, the buffer swap, the physical
-ghost refresh and, for N > 1, the NCCL halo exchange overlapped with the
-interior sweep.
+ghost refresh and, for N > 1, the halo: by default fused into the sweep
+(PSM_HALO=p2p: the kernel stores its boundary planes straight into the
+neighbours' ghost planes over CUDA IPC / NVLink, step flags instead of a
+collective), or PSM_HALO=nccl: NCCL send/recv overlapped with the interior
+sweep.  p2p falls back to nccl when a rank cannot map its neighbours.
 
 Keys beyond the base contract:
   roofline      dominant kernel (line Jacobi sweep) achieved GB/s from 24
@@ -236,13 +239,14 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_1208_1975_b200 as ps
     from paper_1208_1975_b200 import _lib
-    from paper_1208_1975_b200.dist import SlabDomain, dist_smooth, jacobi_step_overlapped
+    from paper_1208_1975_b200.dist import SlabDomain, jacobi_step_overlapped, jacobi_step_p2p, peer_halo
     from paper_1208_1975_b200.smoother import _Plan
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     nx, ny, nz = args.shape
-    dom = SlabDomain((nx, ny, nz), rank, world, device=dev, group=None) if world > 1 else None
+    halo_mode = os.environ.get("PSM_HALO", "p2p")
+    dom = SlabDomain((nx, ny, nz), rank, world, device=dev, group=None, halo=halo_mode) if world > 1 else None
     if dom is None:
         # single GPU: the same class without a process group
         dom = SlabDomain((nx, ny, nz), 0, 1, device=dev)
@@ -264,15 +268,38 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    halo = None
+    if world > 1 and halo_mode == "p2p":
+        ok = 1
+        try:
+            halo = peer_halo(dom, dp)
+        except (_lib.LibraryError, ValueError) as e:  # no IPC mapping: every rank falls back to NCCL
+            print(f"rank {rank}: fused halo unavailable ({e}); using NCCL", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            halo = None
+            dom.halo = halo_mode = "nccl"
+            for side in (0, 1):  # unbind whatever was mapped
+                _lib.check(lib.psm_plan_set_peer_halo(dp.handle, 0, side, None, None, 0), "set_peer_halo")
+            dom._peer = None
+
     # initial ghosts (physical + halo)
     dp.refresh(_lib.GHOST_ALL)
     if world > 1:
         dom.finish_exchange(dom.start_exchange(p._active))
         dom.unpack(dp)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+    nstep = [0]  # p2p: steps since the halo's epoch
 
     def step(s, record):
         # the sweep launches are bracketed by events on the launching stream
-        if world > 1:
+        if halo is not None:
+            jacobi_step_p2p(dom, dp, cfg.omega, s % 2, halo, nstep[0], events=multi_sweeps if record else None)
+            nstep[0] += 1
+        elif world > 1:
             jacobi_step_overlapped(dom, dp, cfg.omega, s % 2, events=multi_sweeps if record else None)
         else:
             _single_step(s)
@@ -311,6 +338,9 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         barrier()
     launches = lib.psm_plan_launches(dp.handle) - launches0
+    if halo is not None:
+        launches += 2 * args.steps  # the flag wait / signal kernels (not counted by the plan)
+        halo.epoch += nstep[0]
     ms = start.elapsed_time(stop)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -318,8 +348,9 @@ def run_ours(args, rank, world, local_rank):
     ms_total = float(t.item())
     cells = nx * ny * nz
     value = cells * args.steps / (ms_total / 1e3) / 1e9
-    # dominant kernel: the sweep (one launch per step on 1 GPU; on N GPUs the
-    # sum of the step's three range launches, the overlapped halo excluded)
+    # dominant kernel: the sweep (one launch per step on 1 GPU and with the
+    # fused halo, its peer stores included; with NCCL the sum of the step's
+    # three range launches, the overlapped halo excluded)
     if sweep_only:
         sweep_ms = sum(a.elapsed_time(b) for a, b in sweep_only) / len(sweep_only)
     else:  # the step's boundary + interior sweep launches, halo excluded
@@ -373,7 +404,11 @@ def run_ours(args, rank, world, local_rank):
                 "block_dims": [nx, 1, 1],
                 "omega": 0.8,
                 "parallelism": f"z-slab x{world}",
-                "step": "sweep (+fused norm, x ghosts) + swap + physical ghosts (+ NCCL halo, overlapped)",
+                "step": "sweep (+fused norm, x ghosts) + swap + physical ghosts" + (
+                    "" if world == 1 else
+                    " + halo fused into the sweep (peer-memory stores, step flags)" if halo is not None else
+                    " + NCCL halo, overlapped"),
+                "halo": None if world == 1 else halo_mode,
                 "l2": "no flush: inputs 25.8 GB per sweep >> 126 MB L2",
             },
             "roofline": roofline,

@@ -129,6 +129,30 @@ int psm_jacobi_sweep_planes(psm_plan* plan, const unsigned char* active, double 
 int psm_halo_unpack(psm_plan* plan, const unsigned char* active, int patch, int side, const double* plane_dev,
                     void* stream);
 
+/* Fused multi-GPU halo over peer memory (z-slabs).  Replaces, for the
+ * cross-rank z interfaces of a slab decomposition, the pack / send / receive /
+ * unpack of exchange_interface_ghosts (grid.py:523-547) with stores the
+ * line-Jacobi sweep itself issues: while it writes plane 0 (nz-1) of a patch
+ * it also writes the same values into the top (bottom) ghost plane of the
+ * lower (upper) neighbour's matching buffer, mapped from another process with
+ * CUDA IPC.  Step protocol per rank (flags are ints in device memory the
+ * neighbours write): psm_halo_wait(my flags >= e + s) -> psm_jacobi_sweep ->
+ * psm_halo_signal(neighbours' flags := e + s + 1) -> swap -> refresh; the
+ * physical ghost fill leaves an interface face's interior alone.
+ *
+ * psm_ipc_get_handle: 64-byte cudaIpcMemHandle of the allocation holding
+ *   `ptr` and the byte offset of `ptr` inside it.
+ * psm_ipc_open_handle: map a peer's handle (cached per handle) -> base+offset.
+ * psm_plan_set_peer_halo: side 0 = the neighbour below (its nz given), 1 =
+ *   above; peer_buf0/1 = its two padded buffers (NULL, NULL clears).  Needs a
+ *   line plan on a z-marching nx (PSM_EUNSUPPORTED otherwise). */
+int psm_ipc_get_handle(const void* ptr, void* handle_out, long long* offset_out);
+int psm_ipc_open_handle(const void* handle, long long offset, void** ptr_out);
+int psm_ipc_close_all(void);
+int psm_plan_set_peer_halo(psm_plan* plan, int patch, int side, double* peer_buf0, double* peer_buf1, int peer_nz);
+int psm_halo_signal(int* flag_a, int* flag_b, int value, void* stream);
+int psm_halo_wait(const int* flags, int n, int value, void* stream);
+
 /* Plane-block solver selection, process-wide: PSM_PLANE_AUTO (default) uses
  * the banded factorised solve (block Thomas along y, Schur complements as
  * short convolutions along x) wherever its truncation bound holds, else the

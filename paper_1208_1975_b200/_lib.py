@@ -54,6 +54,12 @@ EXPORTS = (
     "psm_plan_launches",
     "psm_plane_solver",
     "psm_smooth_steps",
+    "psm_ipc_get_handle",
+    "psm_ipc_open_handle",
+    "psm_ipc_close_all",
+    "psm_plan_set_peer_halo",
+    "psm_halo_signal",
+    "psm_halo_wait",
 )
 PLANE_AUTO = 0
 PLANE_DST = 1
@@ -133,8 +139,16 @@ def load():
             "psm_plan_launches": (ll, [vp]),
             "psm_plane_solver": (i, [i]),
             "psm_smooth_steps": (i, [vp, ub, i, d, i, i, i, vp]),
+            "psm_ipc_get_handle": (i, [vp, vp, ctypes.POINTER(ll)]),
+            "psm_ipc_open_handle": (i, [vp, ll, ctypes.POINTER(vp)]),
+            "psm_ipc_close_all": (i, []),
+            "psm_plan_set_peer_halo": (i, [vp, i, i, vp, vp, i]),
+            "psm_halo_signal": (i, [vp, vp, i, vp]),
+            "psm_halo_wait": (i, [vp, i, i, vp]),
         }
         for name, (res, args) in sig.items():
+            if "PSM_LIB" in os.environ and not hasattr(lib, name):
+                continue  # an older / profiling build named explicitly: bind what it has
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

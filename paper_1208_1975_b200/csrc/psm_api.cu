@@ -26,7 +26,8 @@ bool line_nx_specialised(int nx);
 int zmarch_rows(int nx);
 cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
                                const StencilDev& st, double omega, double* partials, const void* units, int nunits,
-                               int grid, const LineFac& L, cudaStream_t stream, double* rglob = nullptr);
+                               int grid, const LineFac& L, cudaStream_t stream, double* rglob = nullptr,
+                               int peer = 0);
 int line_nx_occupancy(int nx);
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
@@ -41,6 +42,8 @@ cudaError_t launch_tree_sum(const double* in, long long n, double* out, cudaStre
 cudaError_t launch_history_reduce(const PatchDev* patches, int npatch, const double* partials, long long tstride,
                                   int nplanes, int nslots, double* out, cudaStream_t stream);
 cudaError_t launch_halo_unpack(double* dst_plane, const double* src_plane, int px, int py, cudaStream_t stream);
+cudaError_t launch_halo_signal(int* flag_a, int* flag_b, int value, cudaStream_t s);
+cudaError_t launch_halo_wait(const int* flags, int n, int value, cudaStream_t s);
 cudaError_t launch_line_gs(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, int* flags, long long nunits,
                            const int* unit_patch, const int* unit_plane, int threads, size_t smem, int grid,
@@ -676,7 +679,9 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       const char* e = getenv("PSM_ZMARCH_MIN_CELLS");
       return e ? atoll(e) : (1LL << 21);
     }();
-    if (P->tiled && line_nx_specialised(nx) && gcells < zmin) {
+    bool peers = false;  // the fused halo lives in the z-marching kernel only
+    for (int r = p; r < q; ++r) peers |= P->hp[r].iface != 0;
+    if (P->tiled && line_nx_specialised(nx) && gcells < zmin && !peers) {
       // small groups: the one-tile-per-CTA specialised kernel (no TMA ring to
       // fill, no persistent pipeline to drain) is latency-cheaper
       int dev = 0, sms = 148;
@@ -699,7 +704,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms,
-                                   P->fac[p]->h_line, s));
+                                   P->fac[p]->h_line, s, nullptr, peers ? 1 : 0));
       P->launches += 1;
     } else {
       for (int r = p; r < q; ++r) {
@@ -814,6 +819,98 @@ int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int sid
   double* dst = h.buf[a] + (side ? (pz - 1) : 0) * px * py;
   CUDA_TRY(launch_halo_unpack(dst, plane_dev, (int)px, (int)py, (cudaStream_t)stream));
   P->launches += 1;
+  return PSM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused multi-GPU halo over peer memory (z-slabs)
+// ---------------------------------------------------------------------------
+typedef int (*MemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+
+int psm_ipc_get_handle(const void* ptr, void* handle_out, long long* offset_out) {
+  if (!ptr || !handle_out || !offset_out) return fail(PSM_EINVAL, "bad arguments");
+  // the handle names the whole allocation (torch carves tensors out of
+  // larger segments): report the pointer's offset from the allocation base
+  static MemGetAddressRange_t range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (MemGetAddressRange_t)fn;
+  }();
+  if (!range) return fail(PSM_EUNSUPPORTED, "cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)ptr) != 0) return fail(PSM_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+  memcpy(handle_out, &h, sizeof h);
+  *offset_out = (long long)((unsigned long long)ptr - base);
+  return PSM_OK;
+}
+
+static std::map<std::string, void*>& ipc_maps() {
+  static std::map<std::string, void*> m;
+  return m;
+}
+
+int psm_ipc_open_handle(const void* handle, long long offset, void** ptr_out) {
+  if (!handle || !ptr_out || offset < 0) return fail(PSM_EINVAL, "bad arguments");
+  std::string key((const char*)handle, sizeof(cudaIpcMemHandle_t));
+  auto& m = ipc_maps();
+  auto it = m.find(key);
+  void* base = nullptr;
+  if (it != m.end()) {
+    base = it->second;
+  } else {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    m[key] = base;
+  }
+  *ptr_out = (char*)base + offset;
+  return PSM_OK;
+}
+
+int psm_ipc_close_all(void) {
+  auto& m = ipc_maps();
+  for (auto& kv : m) cudaIpcCloseMemHandle(kv.second);
+  m.clear();
+  return PSM_OK;
+}
+
+int psm_plan_set_peer_halo(psm_plan* P, int patch, int side, double* peer_buf0, double* peer_buf1, int peer_nz) {
+  if (!P) return fail(PSM_EINVAL, "null plan");
+  if (patch < 0 || patch >= P->npatch || (side != 0 && side != 1)) return fail(PSM_EINVAL, "bad patch/side");
+  if ((peer_buf0 == nullptr) != (peer_buf1 == nullptr)) return fail(PSM_EINVAL, "give both peer buffers or neither");
+  PatchDev& h = P->hp[patch];
+  if (peer_buf0) {
+    if (P->kind != PSM_BLOCK_LINE || !P->tiled || !line_nx_specialised(h.nx) || h.R != zmarch_rows(h.nx))
+      return fail(PSM_EUNSUPPORTED, "the fused halo needs the z-marching line-Jacobi kernel (nx=%d)", h.nx);
+    if (side == 0 && peer_nz < 1) return fail(PSM_EINVAL, "the lower neighbour's nz must be positive");
+  }
+  if (side == 0) {
+    h.peer_lo[0] = peer_buf0;
+    h.peer_lo[1] = peer_buf1;
+    h.peer_lo_nz = peer_buf0 ? peer_nz : 0;
+  } else {
+    h.peer_hi[0] = peer_buf0;
+    h.peer_hi[1] = peer_buf1;
+  }
+  h.iface = (h.peer_lo[0] ? 1 : 0) | (h.peer_hi[0] ? 2 : 0);
+  CUDA_TRY(cudaMemcpy(P->d_patches + patch, &h, sizeof h, cudaMemcpyHostToDevice));
+  return PSM_OK;
+}
+
+int psm_halo_signal(int* flag_a, int* flag_b, int value, void* stream) {
+  CUDA_TRY(launch_halo_signal(flag_a, flag_b, value, (cudaStream_t)stream));
+  return PSM_OK;
+}
+
+int psm_halo_wait(const int* flags, int n, int value, void* stream) {
+  if (!flags || n < 1 || n > 8) return fail(PSM_EINVAL, "bad flag list");
+  CUDA_TRY(launch_halo_wait(flags, n, value, (cudaStream_t)stream));
   return PSM_OK;
 }
 

@@ -50,11 +50,45 @@ __global__ void __launch_bounds__(256) physical_ghost_kernel(const PatchDev* __r
     if (axis == 0) { i = side ? px - 1 : 0; j = a; k = b; }
     else if (axis == 1) { i = a; j = side ? py - 1 : 0; k = b; }
     else { i = a; j = b; k = side ? pz - 1 : 0; }
+    // the interior of an interface z face belongs to the neighbour's data
+    if (axis == 2 && (P.iface >> side & 1) && i > 0 && i < px - 1 && j > 0 && j < py - 1) continue;
     const int ic = min(max(i, 1), px - 2), jc = min(max(j, 1), py - 2), kc = min(max(k, 1), pz - 2);
     const int flips = (i != ic) + (j != jc) + (k != kc);
     const double val = u[(long long)ic + (long long)px * (jc + (long long)py * kc)];
     u[(long long)i + (long long)px * (j + (long long)py * k)] = (flips & 1) ? -val : val;
   }
+}
+
+// Cross-GPU step signals for the fused halo: after a sweep, publish "my
+// boundary planes of step s are in your ghost planes" into the neighbour's
+// flag word (system-scope release after the sweep's peer stores); before
+// the next sweep, wait until both neighbours published step s.
+__global__ void halo_signal_kernel(int* flag_a, int* flag_b, int value) {
+  __threadfence_system();
+  if (flag_a) asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(flag_a), "r"(value) : "memory");
+  if (flag_b) asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(flag_b), "r"(value) : "memory");
+}
+
+__global__ void halo_wait_kernel(const int* flags, int n, int value) {
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    int v;
+    do {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+      if (clock64() - t0 > (1LL << 36)) __trap();  // a neighbour never signalled (~35 s)
+    } while (v < value);
+  }
+  __threadfence_system();
+}
+
+cudaError_t launch_halo_signal(int* flag_a, int* flag_b, int value, cudaStream_t s) {
+  halo_signal_kernel<<<1, 1, 0, s>>>(flag_a, flag_b, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_wait(const int* flags, int n, int value, cudaStream_t s) {
+  halo_wait_kernel<<<1, 1, 0, s>>>(flags, n, value);
+  return cudaGetLastError();
 }
 
 // Interface ghosts: dst ghost layer <- src interior layer.  Sources are

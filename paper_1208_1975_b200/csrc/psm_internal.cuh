@@ -75,6 +75,14 @@ struct PatchDev {
   const LineFac* lf;
   const PlaneFac* pf;
   const BoxFac* bf;
+  // fused multi-GPU halo (z-slabs): the neighbours' two buffers, mapped over
+  // peer memory; the line-Jacobi sweep stores its first / last plane straight
+  // into their ghost planes.  iface bit 1 / 2: the interior of the z-lo / z-hi
+  // ghost plane is an interface (the physical fill leaves it alone).
+  double* peer_lo[2];
+  double* peer_hi[2];
+  int peer_lo_nz;
+  int iface;
 };
 
 struct CopyDev {

@@ -141,6 +141,10 @@ struct ZAC {
   StencilDev st;
   double omega;
   double *uring, *fring, *rbuf, *wsum, *v;
+  double* peer_lo = nullptr;   // neighbour below: its v buffer (we fill its top ghost plane)
+  double* peer_hi = nullptr;   // neighbour above: its v buffer (we fill its bottom ghost plane)
+  long long peer_lo_off = 0, peer_hi_off = 0;  // added to our v index of plane 0 / nz-1
+  int kw = 0, nz = 0;          // plane phaseC writes, planes of the patch
   double* rg = nullptr;        // RES: global residual of this patch (cell-major like f)
   double* partials = nullptr;  // RES: per (plane, tile) r^2 partials
   long long tslot0 = 0;        // RES: partial index of plane 0's tile
@@ -181,6 +185,26 @@ struct ZAC {
           }
         }
       }
+    // fused halo: a boundary plane also lands in the neighbour's ghost plane
+    // (CTA-uniform and rare, kept out of the loop above)
+    double* pl = kw == 0 ? peer_lo : nullptr;
+    double* ph = kw == nz - 1 ? peer_hi : nullptr;
+    if (RES == 2 && (pl != nullptr || ph != nullptr)) {
+      if (pl) pl += peer_lo_off;
+      if (ph) ph += peer_hi_off;
+#pragma unroll
+      for (int p = 0; p < NXP; ++p)
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int row = trow0 + r, x = tx + p * ACT;
+          if (FULL || row < rows) {
+            const double nv = relax(cold[p * RPT + r], omega, xb[row * RS + x + (x >> 5)]);
+            const long long iu = vbase_old + (long long)row * PX + x;
+            if (pl) pl[iu] = nv;
+            if (ph) ph[iu] = nv;
+          }
+        }
+    }
   }
 
   // plane k: A(k) then C(k-1)
@@ -227,7 +251,7 @@ struct ZAC {
             res = residual7(st, fv, c[i], xl, xr, ym, yp, zm[i], zp[i]);
           }
           ssq = fma(res, res, ssq);
-          if (RES)
+          if (RES == 1)
             __stcs(rg + ((long long)k * ny + j0 + row) * NX + x, res);
           else
             rb[row * RS + x + (x >> 5)] = res;
@@ -242,7 +266,7 @@ struct ZAC {
       mbar_arrive(&empty_u[s_cur]);
       mbar_arrive(&empty_f[t]);
     }
-    if (RES) {
+    if (RES == 1) {
       // residual-only (plane path): the A/C warps reduce the tile partial
       // themselves, in the solver warps' fixed order
       named_sync(kBarRes, ACT);
@@ -257,6 +281,7 @@ struct ZAC {
       if (k > k0) phaseC<FULL>(zm);  // u(k-1) is this plane's zm
     }
     vbase_old = (long long)(k + 1) * pxy + (long long)(j0 + 1) * PX + 1;
+    kw = k;
     s_cur = s_nxt;
     b ^= 1;
   }
@@ -278,11 +303,11 @@ struct ZAC {
     int k = ka;
     for (;;) {
       step<FULL>(A0, A1, A2, k++);
-      if (k >= kb) { if (!RES) phaseC<FULL>(A1); break; }
+      if (k >= kb) { if (RES != 1) phaseC<FULL>(A1); break; }
       step<FULL>(A1, A2, A0, k++);
-      if (k >= kb) { if (!RES) phaseC<FULL>(A2); break; }
+      if (k >= kb) { if (RES != 1) phaseC<FULL>(A2); break; }
       step<FULL>(A2, A0, A1, k++);
-      if (k >= kb) { if (!RES) phaseC<FULL>(A0); break; }
+      if (k >= kb) { if (RES != 1) phaseC<FULL>(A0); break; }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_u[s_cur]);  // the unit's last slab (plane kb)
@@ -290,7 +315,8 @@ struct ZAC {
 };
 
 // RES = 1: residual only (plane path): r = f - A u to rglob plus the tile
-// partials; no solver, no v.
+// partials; no solver, no v.  RES = 2: the sweep plus the fused multi-GPU halo
+// (boundary planes also stored into the z-neighbours' ghost planes).
 template <int NX, int UNIT, int RES>
 __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
     line_jacobi_zmarch_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
@@ -359,7 +385,7 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
 
   // ======================= solver warps ======================================
   if (warp >= C::AC_WARPS) {
-    if (RES) return;
+    if (RES == 1) return;
     const int sl = tid - C::AC_WARPS * 32;  // 0..NSL-1
     const int r = sl / NSEG, s = sl % NSEG;
     const double lo = T.lo, up = T.up, up_h31 = T.up_h31, lo_g0 = T.lo_g0, d_full = T.d_full;
@@ -446,7 +472,15 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
     ac.v = P.buf[active[U.patch] ^ 1];
     ac.j0 = U.j0;
     ac.k0 = U.k0;
-    if (RES) {
+    if (RES == 2) {
+      const int vo = active[U.patch] ^ 1;  // peers swap in lockstep: their v has our parity
+      ac.nz = P.nz;
+      ac.peer_lo = P.peer_lo[vo];
+      ac.peer_hi = P.peer_hi[vo];
+      ac.peer_lo_off = (long long)P.peer_lo_nz * ac.pxy;      // plane 0 -> their plane nz_lo + 1
+      ac.peer_hi_off = -(long long)P.nz * ac.pxy;             // plane nz-1 -> their plane 0
+    }
+    if (RES == 1) {
       ac.rg = rglob + P.cell0;
       ac.tslot0 = P.tile0;
       ac.tpp = P.tpp;
@@ -462,7 +496,7 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
 template <int NX>
 static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                            double omega, double* partials, const ZUnit* units, int nunits, int grid,
-                           const ZTab& T, double* rglob, cudaStream_t stream) {
+                           const ZTab& T, double* rglob, int peer, cudaStream_t stream) {
   using C = ZCfg<NX>;
   static bool attr = false;
   if (!attr) {
@@ -474,6 +508,10 @@ static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned cha
                          (int)C::SMEM_BYTES);
     cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM_BYTES);
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM_BYTES);
+    cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM_BYTES);
     attr = true;
   }
 #define PSM_ZL(U_, R_)                                                                                         \
@@ -482,6 +520,8 @@ static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned cha
                                                                                       rglob)
   if (rglob) {
     if (unit) PSM_ZL(1, 1); else PSM_ZL(0, 1);
+  } else if (peer) {
+    if (unit) PSM_ZL(1, 2); else PSM_ZL(0, 2);
   } else {
     if (unit) PSM_ZL(1, 0); else PSM_ZL(0, 0);
   }
@@ -493,7 +533,7 @@ int zmarch_rows(int nx) { return kMaxTileCells / nx; }
 
 cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const unsigned char* active,
                                const StencilDev& st, double omega, double* partials, const void* units, int nunits,
-                               int grid, const LineFac& L, cudaStream_t stream, double* rglob) {
+                               int grid, const LineFac& L, cudaStream_t stream, double* rglob, int peer) {
   if (nunits <= 0) return cudaSuccess;
   if (grid > nunits) grid = nunits;
   const ZUnit* u = (const ZUnit*)units;
@@ -522,11 +562,11 @@ cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const 
   T.d16 = L.d16;
   }
   switch (nx) {
-    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
-    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
-    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
-    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
-    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, stream);
+    case 64: return zlaunch<64>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, peer, stream);
+    case 128: return zlaunch<128>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, peer, stream);
+    case 256: return zlaunch<256>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, peer, stream);
+    case 512: return zlaunch<512>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, peer, stream);
+    case 1024: return zlaunch<1024>(unit, patches, active, st, omega, partials, u, nunits, grid, T, rglob, peer, stream);
     default: return cudaErrorInvalidValue;
   }
 }

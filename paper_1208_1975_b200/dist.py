@@ -20,6 +20,17 @@ Per Jacobi step on each rank (line blocks), with the halo overlapped:
 
 The exchange helpers are device-agnostic (they move tensors with
 ``torch.distributed``); tests drive them with world_size 2 over gloo on CPU.
+
+Fused halo (``SlabDomain(..., halo="p2p")``, line Jacobi): the neighbours'
+buffers are mapped into this process with CUDA IPC and the sweep kernel itself
+stores its first / last plane into their ghost planes while it writes them, so
+a step is one kernel plus two one-thread flag kernels:
+
+  wait(both neighbours finished step s-1) | sweep (+ peer stores) |
+  signal(step s done) | swap | physical ghosts (interface z faces kept)
+
+No staging buffer, no pack/unpack, no NCCL call on the data path.  The flags
+are ints in device memory (system-scope release / acquire).
 """
 
 from __future__ import annotations
@@ -33,7 +44,8 @@ import torch.distributed as dist
 from . import _lib
 from .grid import Level, Patch, PatchDims, _int3
 
-__all__ = ["slab_range", "SlabDomain", "exchange_planes", "gather_plane_sums", "PatchLevelDomain",
+__all__ = ["slab_range", "SlabDomain", "exchange_planes", "gather_plane_sums", "PatchLevelDomain", "peer_halo",
+           "jacobi_step_p2p",
            "dist_smooth", "dist_smooth_level"]
 
 
@@ -88,18 +100,30 @@ def _exchange_via_host(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank, gro
 
 
 def gather_plane_sums(local, group=None):
-    """All-gather equal-length per-plane vectors (slots, nz_local) in rank
-    order -> (slots, world * nz_local)."""
+    """All-gather per-plane vectors (slots, nz_local) in rank order ->
+    (slots, sum of nz_local).  Ragged slabs (nz not divisible by the rank
+    count) are padded for the collective and cut back after it."""
     world = dist.get_world_size(group)
-    parts = [torch.empty_like(local) for _ in range(world)]
-    dist.all_gather(parts, local.contiguous(), group=group)
-    return torch.cat(parts, dim=-1)
+    n = local.shape[-1]
+    sizes = [torch.empty(1, dtype=torch.int64, device=local.device) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=local.device), group=group)
+    sizes = [int(t.item()) for t in sizes]
+    m = max(sizes)
+    padded = local.new_zeros(local.shape[:-1] + (m,))
+    padded[..., :n] = local
+    parts = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.cat([t[..., :k] for t, k in zip(parts, sizes)], dim=-1)
 
 
 class SlabDomain:
     """This rank's slab of a global grid plus its z-neighbours."""
 
-    def __init__(self, global_shape, rank=None, world=None, device=None, group=None):
+    def __init__(self, global_shape, rank=None, world=None, device=None, group=None, halo="nccl"):
+        if halo not in ("nccl", "p2p"):
+            raise ValueError(f"halo must be 'nccl' or 'p2p', got {halo!r}")
+        self.halo = halo
+        self._peer = None  # _PeerHalo, set up on the first p2p run
         self.global_shape = _int3(global_shape, "global_shape")
         self.rank = dist.get_rank(group) if rank is None else rank
         self.world = dist.get_world_size(group) if world is None else world
@@ -163,6 +187,114 @@ class SlabDomain:
                                            stream), "halo_unpack")
 
 
+class _PeerHalo:
+    """The fused-halo state of one slab: IPC mappings of the z-neighbours'
+    buffers and step flags, bound into the device plan."""
+
+    def __init__(self, domain, dp):
+        lib = _lib.load()
+        p = domain.patch
+        # flags[0] is written by the neighbour below, flags[1] by the one above
+        self.flags = torch.empty(2, dtype=torch.int32, device=p.device)
+        # every rank's earlier signals have landed before any flag is zeroed
+        torch.cuda.synchronize(p.device)
+        dist.barrier(group=domain.group)
+        self.flags.zero_()
+        torch.cuda.synchronize(p.device)
+        try:
+            mine = {"bufs": [_ipc_export(b) for b in p._bufs], "flags": _ipc_export(self.flags),
+                    "nz": domain.nz_local}
+        except (_lib.LibraryError, ValueError) as e:  # still join the gather, so no rank hangs in it
+            mine = {"error": str(e)}
+        allinfo = [None] * domain.world
+        dist.all_gather_object(allinfo, mine, group=domain.group)
+        bad = [f"rank {r}: {i['error']}" for r, i in enumerate(allinfo) if "error" in i]
+        if bad:
+            raise _lib.LibraryError("fused halo: cannot export device buffers (" + "; ".join(bad) + ")")
+        self.peer_flags = [None, None]  # the flag word this rank writes in each neighbour
+        err = ""
+        try:
+            for side, r in ((0, domain.lo_rank), (1, domain.hi_rank)):
+                if r is None:
+                    continue
+                info = allinfo[r]
+                bufs = [_ipc_import(h, off) for h, off in info["bufs"]]
+                flags = _ipc_import(*info["flags"])
+                # below: we are its upper neighbour (its flags[1]); above: its flags[0]
+                self.peer_flags[side] = flags + (4 if side == 0 else 0)
+                _lib.check(lib.psm_plan_set_peer_halo(dp.handle, 0, side, ctypes.c_void_p(bufs[0]),
+                                                      ctypes.c_void_p(bufs[1]), int(info["nz"])), "set_peer_halo")
+        except (_lib.LibraryError, ValueError) as e:
+            err = str(e)
+        errs = [None] * domain.world
+        dist.all_gather_object(errs, err, group=domain.group)
+        if any(errs):
+            for side in (0, 1):
+                lib.psm_plan_set_peer_halo(dp.handle, 0, side, None, None, 0)
+            raise _lib.LibraryError("fused halo unavailable: " + "; ".join(
+                f"rank {r}: {e}" for r, e in enumerate(errs) if e))
+        base = self.flags.data_ptr()
+        if domain.lo_rank is not None and domain.hi_rank is not None:
+            self.wait_ptr, self.nwait = base, 2
+        elif domain.lo_rank is not None:
+            self.wait_ptr, self.nwait = base, 1
+        else:
+            self.wait_ptr, self.nwait = base + 4, 1
+        self.epoch = 0  # flags only grow: value e + s + 1 means step s is done
+        self.handle = dp.handle
+
+    def wait(self, value, stream):
+        _lib.check(_lib.load().psm_halo_wait(ctypes.c_void_p(self.wait_ptr), self.nwait, int(value), stream),
+                   "halo_wait")
+
+    def signal(self, value, stream):
+        a, b = self.peer_flags
+        _lib.check(_lib.load().psm_halo_signal(ctypes.c_void_p(a), ctypes.c_void_p(b), int(value), stream),
+                   "halo_signal")
+
+
+def _ipc_export(t):
+    lib = _lib.load()
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_longlong()
+    _lib.check(lib.psm_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)), "ipc_get_handle")
+    return bytes(h), off.value
+
+
+def _ipc_import(handle, offset):
+    lib = _lib.load()
+    ptr = ctypes.c_void_p()
+    _lib.check(lib.psm_ipc_open_handle(ctypes.c_char_p(handle), int(offset), ctypes.byref(ptr)), "ipc_open_handle")
+    return ptr.value
+
+
+def peer_halo(domain, dp):
+    """The domain's fused-halo state bound to device plan ``dp`` (created,
+    and the IPC handles exchanged, on first use; collective)."""
+    if domain._peer is None or domain._peer.handle != dp.handle:
+        domain._peer = _PeerHalo(domain, dp)
+    return domain._peer
+
+
+def jacobi_step_p2p(domain, dp, omega, slot, halo, step, events=None):
+    """One line-Jacobi step of a slab with the fused peer-memory halo (see
+    the module docstring).  ``step`` counts from 0 within the current run."""
+    p = domain.patch
+    stream = ctypes.c_void_p(torch.cuda.current_stream(p.device).cuda_stream)
+    halo.wait(halo.epoch + step, stream)
+    if events is not None:
+        a = torch.cuda.Event(enable_timing=True)
+        a.record(torch.cuda.current_stream(p.device))
+    dp.jacobi(omega, slot)
+    if events is not None:
+        b = torch.cuda.Event(enable_timing=True)
+        b.record(torch.cuda.current_stream(p.device))
+        events.append([(a, b)])
+    halo.signal(halo.epoch + step + 1, stream)
+    p.swap_buffers()
+    dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+
+
 def dist_smooth(domain, config, cache, record_history=True):
     """``smooth`` on a z-slab decomposed grid: every rank calls it with its
     own ``SlabDomain``; returns the (global) history on every rank."""
@@ -174,13 +306,29 @@ def dist_smooth(domain, config, cache, record_history=True):
     lib = _lib.load()
     steps = config.steps
     nzl = domain.nz_local
+    fused = domain.halo == "p2p" and config.scheme == "block_jacobi" and plan.kind == "line" and domain.world > 1
     with torch.cuda.device(plan.device):
+        halo = None
+        if fused:
+            try:  # collective; raises on every rank alike
+                halo = peer_halo(domain, dp)
+            except _lib.LibraryError:
+                fused = False  # this plan cannot take the fused halo: NCCL overlap
         dp.reserve(steps + 1)
         dp.refresh(_lib.GHOST_ALL)
         reqs = domain.start_exchange(domain.patch._active)
         domain.finish_exchange(reqs)
         domain.unpack(dp)
-        if config.scheme == "block_jacobi" and plan.kind == "line":
+        if fused:
+            torch.cuda.synchronize(plan.device)
+            dist.barrier(group=domain.group)
+            stream = ctypes.c_void_p(torch.cuda.current_stream(plan.device).cuda_stream)
+            for s in range(steps):
+                jacobi_step_p2p(domain, dp, config.omega, s, halo, s)
+            halo.wait(halo.epoch + steps, stream)  # the neighbours' last planes are in
+            halo.epoch += steps
+            dp.residual(steps)
+        elif config.scheme == "block_jacobi" and plan.kind == "line":
             for s in range(steps):
                 jacobi_step_overlapped(domain, dp, config.omega, s)
             dp.residual(steps)

@@ -172,3 +172,37 @@ def test_patch_partition_exchange_fills_cross_rank_ghosts(tmp_path):
         np.testing.assert_array_equal(dst[d], src[s])
         checked += 1
     assert checked > 0
+
+
+def test_slab_domain_halo_modes():
+    from paper_1208_1975_b200.dist import SlabDomain
+
+    d = SlabDomain((8, 4, 6), rank=1, world=2, device="cpu", halo="p2p")
+    assert d.halo == "p2p" and d._peer is None and (d.k0, d.k1) == (3, 6)
+    with pytest.raises(ValueError):
+        SlabDomain((8, 4, 6), rank=0, world=2, device="cpu", halo="shm")
+
+
+def _ragged_main(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1208_1975_b200.dist import gather_plane_sums, slab_range
+
+        k0, k1 = slab_range(17, world, rank)
+        local = torch.arange(k0, k1, dtype=torch.float64)[None, :].repeat(2, 1) + 100.0 * torch.arange(2)[:, None]
+        full = gather_plane_sums(local)
+        np.save(os.path.join(out_dir, f"g{rank}.npy"), full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_plane_sums_ragged_slabs(tmp_path):
+    """17 planes over 3 ranks (6, 6, 5): the gathered per-plane vector is the
+    global one in plane order, no padding left in it."""
+    world = 3
+    mp.spawn(_ragged_main, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    want = np.arange(17, dtype=np.float64)[None, :] + 100.0 * np.arange(2)[:, None]
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"g{r}.npy"), want)
