@@ -29,6 +29,10 @@ cudaError_t launch_line_zmarch(int nx, int unit, const PatchDev* patches, const 
                                int grid, const LineFac& L, cudaStream_t stream, double* rglob = nullptr,
                                int peer = 0);
 int line_nx_occupancy(int nx);
+bool line_zgen_supported(int nx);
+cudaError_t launch_line_zgen(const int* nxs, int nnx, int unit, const PatchDev* patches, const unsigned char* active,
+                             const StencilDev& st, double omega, double* partials, const void* units, int nunits,
+                             int grid, const LineFac& L, cudaStream_t stream);
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
                            cudaStream_t stream);
@@ -622,7 +626,8 @@ static int zmarch_units(psm_plan* P, int p0, int p1, int ka, int kb, void** d_un
   }
   long long cols = 0;
   for (int p = p0; p < p1; ++p) cols += P->hp[p].tpp;
-  const long long planes = std::max(1, (kb < 0 ? P->hp[p0].nz : kb) - ka);
+  long long planes = 1;  // the deepest patch's plane range
+  for (int p = p0; p < p1; ++p) planes = std::max<long long>(planes, (kb < 0 ? P->hp[p].nz : kb) - ka);
   // plane-chunk length: minimise the busiest persistent CTA's work,
   // ceil(units / SMs) * (chunk + ~2 planes of halo and pipeline fill)
   int dev = 0, sms = 148;
@@ -658,6 +663,31 @@ static int zmarch_units(psm_plan* P, int p0, int p1, int ka, int kb, void** d_un
   *d_units = d;
   *nunits = (int)(u.size() / 4);
   return PSM_OK;
+}
+
+// 16-byte aligned buffers of every patch in [p, q) (the bulk copies' rule)
+static bool group_aligned(const psm_plan* P, int p, int q) {
+  for (int r = p; r < q; ++r) {
+    const PatchDev& h = P->hp[r];
+    if (((uintptr_t)h.buf[0] | (uintptr_t)h.buf[1] | (uintptr_t)h.f) & 15) return false;
+  }
+  return true;
+}
+
+// patch p can take the runtime-nx z-marching kernel
+static bool zgen_ok(const psm_plan* P, int p) {
+  const PatchDev& h = P->hp[p];
+  return P->tiled && !line_nx_specialised(h.nx) && line_zgen_supported(h.nx) && group_aligned(P, p, p + 1);
+}
+
+// cells of planes [ka, kb) over the run of zgen-eligible patches from p (end -> *q)
+static long long zgen_cells(const psm_plan* P, int p, int pb, int ka, int kb, int* q) {
+  long long cells = 0;
+  int r = p;
+  for (; r < pb && zgen_ok(P, r); ++r)
+    cells += (long long)P->hp[r].nx * P->hp[r].ny * ((kb < 0 ? P->hp[r].nz : kb) - ka);
+  *q = r;
+  return cells;
 }
 
 // Line-Jacobi sweep of planes [ka, kb) (kb < 0: all planes) of patches
@@ -705,6 +735,33 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms,
                                    P->fac[p]->h_line, s, nullptr, peers ? 1 : 0));
+      P->launches += 1;
+    } else if (zgen_ok(P, p) && zgen_cells(P, p, pb, ka, kb, &q) >= zmin) {
+      // other even nx: the z-marching pipeline with the line length per unit,
+      // one launch over consecutive such patches whatever their nx
+      void* units;
+      int nu;
+      int rc = zmarch_units(P, p, q, ka, kb, &units, &nu);
+      if (rc) return rc;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      std::vector<int> nxs;
+      for (int r = p; r < q; ++r) nxs.push_back(P->hp[r].nx);
+      CUDA_TRY(launch_line_zgen(nxs.data(), (int)nxs.size(), unit ? 1 : 0, P->d_patches, da, P->st, omega, part,
+                                units, nu, sms, P->fac[p]->h_line, s));
+      P->launches += 1;
+    } else if (ka == 0 && kb < 0) {
+      // whole-patch sweeps of consecutive patches the specialised kernels do
+      // not cover (any nx) are one launch over their contiguous tile range
+      while (q < pb && !(P->tiled && line_nx_specialised(P->hp[q].nx))) ++q;
+      const long long t0 = P->hp[p].tile0, nt = P->hp[q - 1].tile0 + P->hp[q - 1].tiles - t0;
+      if (P->tiled) {
+        CUDA_TRY(launch_line_tiles(1, P->d_patches, P->npatch, da, P->st, omega, part, nullptr, t0, nt, P->threads,
+                                   P->smem, s));
+      } else {
+        CUDA_TRY(launch_line_generic(1, P->d_patches, P->npatch, da, P->st, omega, part, t0, nt, s));
+      }
       P->launches += 1;
     } else {
       for (int r = p; r < q; ++r) {

@@ -85,6 +85,11 @@ CONFIGS = {
                build=lambda: ps.build_level([(512, 512, 512)]),
                runs=[("block_jacobi", (8, 8, 8), None), ("block_jacobi", (4, 4, 4), None),
                      ("block_jacobi", (2, 2, 2), None), ("chaotic_block_gs", (8, 8, 8), "wavefront")]),
+    "F3": dict(desc="SURVEY f3 / paper Table 2: mixed set, 16 patches each of 64^3..96^3 abutting along x",
+               build=lambda: ps.build_patch_set(ps.PatchSetSpec.mixed_table2()),
+               runs=[("block_jacobi", (96, 1, 1), None), ("chaotic_block_gs", (96, 1, 1), "wavefront"),
+                     ("chaotic_block_gs", (96, 1, 1), "chaotic"), ("block_jacobi", (96, 96, 1), None),
+                     ("block_jacobi", (8, 8, 8), None)]),
     "C5": dict(desc="1024^3 uniform grid, line Jacobi, 1 GPU",
                build=lambda: ps.build_level([(1024, 1024, 1024)]), runs=[("block_jacobi", "line", None)]),
 }
@@ -108,8 +113,10 @@ def main():
         for ri, (scheme, kind, mode) in enumerate(C["runs"]):
             if ri not in sel:
                 continue
-            if isinstance(kind, tuple):  # box blocks
-                bd, kind = kind, "box" + "x".join(str(b) for b in kind)
+            if isinstance(kind, tuple):  # explicit block dims
+                bd = kind
+                kind = ("line" if kind[1:] == (1, 1) else "plane" if kind[2] == 1 else
+                        "box" + "x".join(str(b) for b in kind))
             else:
                 bd = (p0.nx, 1, 1) if kind == "line" else (p0.nx, p0.ny, 1)
             solver = "dst" if mode == "dst" else "auto"
