@@ -368,8 +368,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll
           for (int i = 0; i < kSeg; ++i) y[i] = i < len ? seg[i] * T.invm[i] : 0.0;
 #pragma unroll
-          for (int i = 1; i < kSeg; ++i)
-            if (i < len) y[i] = fma(-T.loinv[i], y[i - 1], y[i]);
+          for (int i = 1; i < kSeg; ++i)  // past a tail's end the input is 0: harmless, no select
+            y[i] = fma(-T.loinv[i], y[i - 1], y[i]);
 #pragma unroll
           for (int i = kSeg - 2; i >= 0; --i)
             if (i < len - 1) y[i] = fma(-T.cp[i], y[i + 1], y[i]);
