@@ -807,12 +807,15 @@ int psm_plane_residual(psm_plan* P, const unsigned char* da, double* partials, d
                                   rbuf));
       P->launches += 1;
     } else {
-      for (int r = p; r < q; ++r) {
-        const PatchDev& h = P->hp[r];
-        CUDA_TRY(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, rbuf, h.tile0, h.tiles,
-                                   P->threads, 0, s));
-        P->launches += 1;
-      }
+      // consecutive patches without the z-marching kernel: one launch over
+      // their contiguous tile range
+      while (q < P->npatch &&
+             !(P->tiled && line_nx_specialised(P->hp[q].nx) && P->hp[q].R == zmarch_rows(P->hp[q].nx)))
+        ++q;
+      const long long t0 = P->hp[p].tile0, nt = P->hp[q - 1].tile0 + P->hp[q - 1].tiles - t0;
+      CUDA_TRY(launch_line_tiles(2, P->d_patches, P->npatch, da, P->st, 0.0, partials, rbuf, t0, nt, P->threads, 0,
+                                 s));
+      P->launches += 1;
     }
     p = q;
   }

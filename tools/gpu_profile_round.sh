@@ -10,7 +10,7 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
   python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
 python tools/launch_summary.py $O/launches_bench.csv > $O/launches_bench.txt 2>&1
 timeout -s KILL 300 python __graft_entry__.py > $O/smoke.log 2>&1; echo "smoke rc=$?"
-for c in C2 C3 C4 F1; do
+for c in C2 C3 C4 F1 F3; do
   timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$c.csv \
     python tools/bench_configs.py --only $c --steps 1 --warmup 1 > /dev/null 2>&1
   python tools/launch_summary.py $O/launches_$c.csv > $O/launches_$c.txt 2>&1
@@ -24,7 +24,12 @@ timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k re
 bash tools/ncu_plane.sh 512 round/plane_band_512 > /dev/null 2>&1; echo "ncu band rc=$?"
 bash tools/ncu_box.sh 512 8 round/box_8_512 > /dev/null 2>&1; echo "ncu box rc=$?"
 bash tools/ncu_line.sh 1024 round/line_jacobi_1024 > /dev/null 2>&1; echo "ncu line rc=$?"
-for r in gs_pipe_256 plane_band_512 box_8_512 line_jacobi_1024; do
+bash tools/ncu_zgen.sh round/line_zgen_f3 > /dev/null 2>&1; echo "ncu zgen rc=$?"
+# the fused peer-memory halo: 2 ranks sharing this one GPU (IPC), gloo for the plumbing
+PSM_HALO=p2p PSM_DIST_BACKEND=gloo timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29613 bench.py --gpus 2 --steps 10 --warmup 3 --shape 512 512 512 \
+  --no-cpu-baseline > $O/bench_p2p_2ranks_1gpu.json 2> $O/bench_p2p.err; echo "p2p rc=$?"
+for r in gs_pipe_256 plane_band_512 box_8_512 line_jacobi_1024 line_zgen_f3; do
   python tools/ncu_summary.py $O/$r.ncu-rep > $O/${r}_summary.txt 2>&1
 done
 echo done
