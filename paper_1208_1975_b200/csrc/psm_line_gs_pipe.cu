@@ -2,8 +2,9 @@
 //
 // Replaces smoother._gs_step + block_residual + block_update/matvec for line
 // blocks (smoother.py:156-169, stencil.py:93-112, blocklinalg.py:90-105) when
-// nx is 32, 64, 128 or 256.  Ghosts are lagged until the step-end refresh,
-// as in the reference.
+// nx is even and splits into nl <= 32 lane chunks of NC <= 8 cells (32, 64,
+// 128, 256 with all 32 lanes; 72 = 24 x 3, 80 = 20 x 4, ...).  Ghosts are
+// lagged until the step-end refresh, as in the reference.
 //
 // Order.  The serial strategy visits x-lines (j,k) of a patch
 // lexicographically, j fastest (runtime.py:164-168): line (j,k) reads the NEW
@@ -18,7 +19,8 @@
 // memory ordering, the contract of smooth_chaotic_gs_step under parallel
 // strategies.
 //
-// Line solve.  Lane L owns the NC = nx/32 contiguous cells L*NC .. L*NC+NC-1.
+// Line solve.  Lane L < nl owns the NC = nx/nl contiguous cells L*NC .. L*NC+NC-1
+// (lanes nl..31 own none and carry identity rows of the interface system).
 // Cells 0..NC-2 of a chunk are eliminated locally (constant Thomas factors and
 // spikes g, h: one set serves every chunk), which leaves one tridiagonal
 // interface system in the chunks' last cells a_L.  That 32-unknown system is
@@ -58,7 +60,7 @@ struct GsUniform {
 template <int NC>
 struct GCfg {
   static constexpr int IS = 32 + 16 / NC;      // stride between the NC "i-rows" of a slot
-  static constexpr int SLOT = NC * IS + 2;     // doubles per ring slot (+ the two x-ghosts)
+  static constexpr int SLOT = (NC * IS + 3) / 2 * 2;  // doubles per ring slot (+ the two x-ghosts), even: 16-B bulk copies
   static constexpr int D = 3;                  // prefetch ring depth
   static constexpr int P = D - 1;              // rows of prefetch ahead
   static constexpr int DH = 2;                 // new-row ring depth (warp -> next warp)
@@ -169,10 +171,10 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
     line_gs_pipe_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
                         StencilDev st, double omega, int* __restrict__ flags, int* __restrict__ ticket,
                         const int2* __restrict__ units, int nunits, const double* __restrict__ lane_tab,
-                        const __grid_constant__ GsUniform T) {
+                        const __grid_constant__ GsUniform T, int nl) {
   using C = GCfg<NC>;
   constexpr int M = NC - 1;  // locally eliminated cells per chunk
-  constexpr int nx = 32 * NC;
+  const int nx = NC * nl;    // lanes nl..31 carry no cells (nx not 32*NC)
   constexpr int IS = C::IS, SLOT = C::SLOT, D = C::D, P = C::P, DH = C::DH, DHL = C::DHL, DM = C::DM;
   constexpr int MROW = C::MROW;
   extern __shared__ __align__(16) double gsm[];
@@ -236,7 +238,8 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           const double* hs = HL + s * SLOT;
           double* dst = row0 + (long long)j * px;
 #pragma unroll
-          for (int i = 0; i < NC; ++i) __stcg(dst + i * 32 + lane, hs[dpos[i]]);
+          for (int i = 0; i < NC; ++i)
+            if (i * 32 + lane < nx) __stcg(dst + i * 32 + lane, hs[dpos[i]]);
           __syncwarp();
           if (lane == 0) {
             gs_mbar_arrive(&emptyL[s]);
@@ -266,14 +269,17 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
 #pragma unroll
           for (int i = 0; i < NC; ++i) {
             const int x = i * 32 + lane;
-            cp_async8(Ur + s + dpos[i], src_u + x);
-            cp_async8(Zr + s + dpos[i], src_z + x);
-            cp_async8(Fr + s + dpos[i], src_f + x);
+            if (x < nx) {
+              cp_async8(Ur + s + dpos[i], src_u + x);
+              cp_async8(Zr + s + dpos[i], src_z + x);
+              cp_async8(Fr + s + dpos[i], src_f + x);
+            }
           }
           if (warp == 0 && k == 0) {
             const double* src_m = src_u - px - pxy;
 #pragma unroll
-            for (int i = 0; i < NC; ++i) cp_async8(Mr + s + dpos[i], src_m + i * 32 + lane);
+            for (int i = 0; i < NC; ++i)
+              if (i * 32 + lane < nx) cp_async8(Mr + s + dpos[i], src_m + i * 32 + lane);
           }
           if (lane < 2) cp_async8(Ur + s + NC * IS + lane, src_u - px + (lane ? nx : -1));
         }
@@ -283,8 +289,8 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
       double cen[NC], ym[NC];
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
-        cen[i] = row0[lane * NC + i];
-        ym[i] = row0[lane * NC + i - px];
+        cen[i] = lane < nl ? row0[lane * NC + i] : 0.0;
+        ym[i] = lane < nl ? row0[lane * NC + i - px] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < P; ++j) issue(j);
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
 #pragma unroll
           for (int i = 0; i < NC; ++i) {
             const double xl = i > 0 ? cen[i > 0 ? i - 1 : 0] : (lane == 0 ? gl : lft);
-            const double xr = i < NC - 1 ? cen[i < NC - 1 ? i + 1 : 0] : (lane == 31 ? gr : rgt);
+            const double xr = i < NC - 1 ? cen[i < NC - 1 ? i + 1 : 0] : (lane == nl - 1 ? gr : rgt);
             if (UNIT) {  // faces all -1: face*nbr is exactly -nbr, same roundings
               double a = __dmul_rn(st.c, cen[i]);
               a = __dsub_rn(a, xl);
@@ -360,8 +366,9 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
             const int lim = min(avail, j + DM);
             for (; issued < lim; ++issued) {
               const uint32_t n = mbase + (uint32_t)issued;
-              gs_mbar_expect_tx(&mbarM[n % DM], MROW * 8);
-              gs_tma_row(Mr + (n % DM) * MROW, row0 + (long long)issued * px - pxy - 1, MROW * 8, &mbarM[n % DM]);
+              gs_mbar_expect_tx(&mbarM[n % DM], (uint32_t)(px * 8));
+              gs_tma_row(Mr + (n % DM) * MROW, row0 + (long long)issued * px - pxy - 1, (uint32_t)(px * 8),
+                         &mbarM[n % DM]);
             }
           }
           __syncwarp();
@@ -381,6 +388,7 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
             const double a = __dadd_rn(acc[i], __dmul_rn(st.zm, zm[i]));
             r[i] = __dsub_rn(fv[i], __dadd_rn(a, __dmul_rn(st.zp, zp[i])));
           }
+          if (lane >= nl) r[i] = 0.0;  // cell-less lanes: identity rows of the interface system
         }
         GS_PROF(4, r[NC - 1] + r[0]);
         // ---- exact line solve: local elimination + PCR ------------------
@@ -439,7 +447,8 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           if (consumer && lane == 0) gs_mbar_arrive(&fullH[warp * DH + hs]);
           double* dst = row0 + (long long)j * px;
 #pragma unroll
-          for (int i = 0; i < NC; ++i) __stcg(dst + i * 32 + lane, h[dpos[i]]);
+          for (int i = 0; i < NC; ++i)
+            if (i * 32 + lane < nx) __stcg(dst + i * 32 + lane, h[dpos[i]]);
         }
         issue(j + P);  // prefetch, off the hand-off critical path
         GS_PROF(8, 0.0);
@@ -474,11 +483,11 @@ template <int NC>
 static cudaError_t gs_pipe_launch(int chaotic, int unit, int grid, const PatchDev* patches,
                                   const unsigned char* active, const StencilDev& st, double omega, int* flags,
                                   int* ticket, const int2* units, int nunits, const double* lane_tab,
-                                  const GsUniform& T, cudaStream_t s) {
+                                  const GsUniform& T, int nl, cudaStream_t s) {
   using C = GCfg<NC>;
 #define PSM_GSP(CH, UN)                                                                                     \
   line_gs_pipe_kernel<NC, CH, UN><<<grid, kGsThreads, C::SMEM, s>>>(patches, active, st, omega, flags, ticket, \
-                                                                    units, nunits, lane_tab, T)
+                                                                    units, nunits, lane_tab, T, nl)
   if (chaotic) {
     if (unit) PSM_GSP(1, 1); else PSM_GSP(1, 0);
   } else {
@@ -494,9 +503,9 @@ using namespace psm;
 
 int psm_set_error(int code, const char* msg);
 
-// One group of patches sharing nx (= 32*NC): units, tables, launch geometry.
+// One group of patches sharing nx (= NC * nl): units, tables, launch geometry.
 struct GsPipeGroup {
-  int nc = 0;
+  int nc = 0, nl = 32;
   int2* d_units = nullptr;
   int nunits = 0;
   double* d_tab = nullptr;  // [kGsTab][32]
@@ -521,11 +530,24 @@ extern "C" int psm_debug_gs_profile(long long* out, int reset) {
 }
 #endif
 
-bool gs_pipe_supported(int nx) { return nx == 32 || nx == 64 || nx == 128 || nx == 256; }
+// Chunk length for a line of nx cells: the smallest NC <= 8 dividing nx with
+// nx / NC <= 32 lanes (32, 64, 128, 256 -> 1, 2, 4, 8 and all 32 lanes;
+// e.g. 72 -> 3 x 24 lanes, 80 -> 4 x 20); 0 when there is none.  nx must be
+// even: warp 0 pulls whole padded rows with 16-byte bulk copies.
+static int gs_pipe_nc(int nx) {
+  if (nx < 2 || (nx & 1)) return 0;
+  for (int nc = 1; nc <= 8; ++nc)
+    if (nx % nc == 0 && nx / nc <= 32) return nc;
+  return 0;
+}
 
-// Host tables (long double) for the chunked line solve of order nx = 32*nc
-// with sub-diagonal lo, diagonal d and super-diagonal up.
-static int gs_pipe_tables(int nc, long double lo, long double d, long double up, GsUniform& T, double* lane_tab) {
+bool gs_pipe_supported(int nx) { return gs_pipe_nc(nx) > 0; }
+
+// Host tables (long double) for the chunked line solve of order nx = nc*nl
+// with sub-diagonal lo, diagonal d and super-diagonal up; lanes nl..31 get
+// identity rows.
+static int gs_pipe_tables(int nc, int nl, long double lo, long double d, long double up, GsUniform& T,
+                          double* lane_tab) {
   const int m = nc - 1;
   memset(&T, 0, sizeof T);
   long double invm[8] = {0}, cp[8] = {0}, g[8] = {0}, h[8] = {0};
@@ -567,22 +589,27 @@ static int gs_pipe_tables(int nc, long double lo, long double d, long double up,
   // interface system  A_L a_{L-1} + B_L a_L + C_L a_{L+1} = rhs_L
   long double A[32], B[32], Cc[32];
   for (int L = 0; L < 32; ++L) {
-    if (m == 0) {
+    if (L >= nl) {  // no cells: a_L = 0
+      A[L] = 0.0L;
+      B[L] = 1.0L;
+      Cc[L] = 0.0L;
+    } else if (m == 0) {
       A[L] = L > 0 ? lo : 0.0L;
       B[L] = d;
-      Cc[L] = L < 31 ? up : 0.0L;
+      Cc[L] = L < nl - 1 ? up : 0.0L;
     } else {
       A[L] = L > 0 ? -lo * g[m - 1] : 0.0L;
-      B[L] = d - lo * h[m - 1] - (L < 31 ? up * g[0] : 0.0L);
-      Cc[L] = L < 31 ? -up * h[0] : 0.0L;
+      B[L] = d - lo * h[m - 1] - (L < nl - 1 ? up * g[0] : 0.0L);
+      Cc[L] = L < nl - 1 ? -up * h[0] : 0.0L;
     }
-    if (fabsl(B[L]) < 1e-14L * fabsl(d)) return psm_set_error(PSM_ESINGULAR, "line interface pivot below 1e-14*|A|");
+    if (L < nl && fabsl(B[L]) < 1e-14L * fabsl(d))
+      return psm_set_error(PSM_ESINGULAR, "line interface pivot below 1e-14*|A|");
   }
   long double al[32], ga[32];
   for (int L = 0; L < 32; ++L) {
     lane_tab[0 * 32 + L] = (double)(1.0L / B[L]);
-    lane_tab[1 * 32 + L] = m > 0 ? (double)(lo / B[L]) : 0.0;
-    lane_tab[2 * 32 + L] = (m > 0 && L < 31) ? (double)(up / B[L]) : 0.0;
+    lane_tab[1 * 32 + L] = (m > 0 && L < nl) ? (double)(lo / B[L]) : 0.0;
+    lane_tab[2 * 32 + L] = (m > 0 && L < nl - 1) ? (double)(up / B[L]) : 0.0;
     al[L] = A[L] / B[L];
     ga[L] = Cc[L] / B[L];
   }
@@ -623,7 +650,16 @@ int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  for (int nc : {1, 2, 4, 8}) {
+  std::vector<int> nxs;
+  for (int p = 0; p < P->npatch; ++p) nxs.push_back(P->hp[p].nx);
+  std::sort(nxs.begin(), nxs.end());
+  nxs.erase(std::unique(nxs.begin(), nxs.end()), nxs.end());
+  for (int nx : nxs) {
+    const int nc = gs_pipe_nc(nx);
+    if (nc == 0) {
+      delete S;
+      return psm_set_error(PSM_EUNSUPPORTED, "line GS pipeline: unsupported nx");
+    }
     // units (patch, k0) plane-group-major: every patch's first group comes
     // before any second group, so independent patches fill the machine while
     // each patch's CTA chain (group k0 waits on group k0-W) stays in order
@@ -632,16 +668,17 @@ int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets) {
     for (int p = 0; p < P->npatch; ++p) maxnz = std::max(maxnz, P->hp[p].nz);
     for (int k0 = 0; k0 < maxnz; k0 += kGsW)
       for (int p = 0; p < P->npatch; ++p) {
-        if (P->hp[p].nx != 32 * nc || k0 >= P->hp[p].nz) continue;
+        if (P->hp[p].nx != nx || k0 >= P->hp[p].nz) continue;
         uv.push_back(p);
         uv.push_back(k0);
       }
     if (uv.empty()) continue;
     GsPipeGroup G;
     G.nc = nc;
+    G.nl = nx / nc;
     G.nunits = (int)(uv.size() / 2);
     double tab[kGsTab * 32];
-    int rc = gs_pipe_tables(nc, (long double)P->st.xm, (long double)P->st.c, (long double)P->st.xp, G.T, tab);
+    int rc = gs_pipe_tables(nc, G.nl, (long double)P->st.xm, (long double)P->st.c, (long double)P->st.xp, G.T, tab);
     if (rc) {
       delete S;
       return rc;
@@ -657,7 +694,11 @@ int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets) {
     switch (nc) {
       case 1: occ = gs_pipe_occupancy<1>(); break;
       case 2: occ = gs_pipe_occupancy<2>(); break;
+      case 3: occ = gs_pipe_occupancy<3>(); break;
       case 4: occ = gs_pipe_occupancy<4>(); break;
+      case 5: occ = gs_pipe_occupancy<5>(); break;
+      case 6: occ = gs_pipe_occupancy<6>(); break;
+      case 7: occ = gs_pipe_occupancy<7>(); break;
       default: occ = gs_pipe_occupancy<8>(); break;
     }
     if (occ < 1) {
@@ -692,12 +733,20 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
   for (const GsPipeGroup& G : P->gspipe->groups) {
     cudaError_t e;
     int* tk = tickets + G.ticket;
+#define PSM_GSL(N) \
+  gs_pipe_launch<N>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, \
+                    G.T, G.nl, s)
     switch (G.nc) {
-      case 1: e = gs_pipe_launch<1>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
-      case 2: e = gs_pipe_launch<2>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
-      case 4: e = gs_pipe_launch<4>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
-      default: e = gs_pipe_launch<8>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, G.T, s); break;
+      case 1: e = PSM_GSL(1); break;
+      case 2: e = PSM_GSL(2); break;
+      case 3: e = PSM_GSL(3); break;
+      case 4: e = PSM_GSL(4); break;
+      case 5: e = PSM_GSL(5); break;
+      case 6: e = PSM_GSL(6); break;
+      case 7: e = PSM_GSL(7); break;
+      default: e = PSM_GSL(8); break;
     }
+#undef PSM_GSL
     if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
     P->launches += 1;
   }

@@ -1,5 +1,5 @@
-"""Parity of the plane-pipelined line GS kernel (psm_line_gs_pipe.cu: nx in
-{32, 64, 128, 256}) with the CPU restatement of the reference's serial
+"""Parity of the plane-pipelined line GS kernel (psm_line_gs_pipe.cu: even nx
+that splits into <= 32 lane chunks of <= 8 cells) with the CPU restatement of the reference's serial
 (lexicographic) block GS, through the public API.
 
 Wavefront ("colour-ordered") mode: iterates and histories within 1e-12
@@ -109,6 +109,42 @@ def test_wavefront_gs_mixed_line_lengths():
 @pytest.mark.parametrize("shape", [(128, 64, 40), (256, 32, 24)])
 def test_chaotic_gs_factor_within_two_percent_of_serial(shape):
     o, g = _pair([(shape, (0, 0, 0))], seed=9)
+    want, hist = _run(o, g, steps=4, mode="chaotic")
+    for s in range(1, len(want)):
+        got_f, ref_f = hist[s] / hist[s - 1], want[s] / want[s - 1]
+        assert abs(got_f - ref_f) / ref_f < 0.02, (s, got_f, ref_f)
+
+
+@pytest.mark.parametrize(
+    "shape",
+    # nx = nl lanes x NC cells with nl < 32 or NC not a power of two
+    [(72, 20, 15), (80, 17, 9), (88, 12, 10), (96, 9, 16), (12, 10, 8), (42, 7, 5), (150, 8, 9), (180, 6, 7),
+     (210, 5, 8), (200, 4, 11), (2, 5, 4), (24, 1, 9)],
+)
+def test_wavefront_gs_general_line_lengths(shape):
+    o, g = _pair([(shape, (0, 0, 0))], seed=7 + sum(shape))
+    want, hist = _run(o, g, steps=2)
+    assert G.rel_maxnorm(g.patches[0].u.cpu().numpy(), o.patches[0].u) < TOL
+    assert G.hist_rel(hist, want) < TOL
+
+
+def test_wavefront_gs_mixed_table2_like_level():
+    """Patches of the paper's mixed sizes' line lengths (64..96), abutting
+    along x with partial faces: one pipelined group per nx."""
+    so = [((64, 8, 9), (0, 0, 0)), ((72, 9, 10), (64, 0, 0)), ((80, 10, 8), (136, 0, 0)),
+          ((88, 8, 11), (216, 1, 0)), ((96, 11, 9), (304, 0, 0))]
+    o, g = _pair(so, seed=13)
+    want = R.smooth(o, "chaotic_block_gs", (96, 1, 1), steps=2, exact_norm=False)
+    cfg = ps.SmootherConfig(scheme="chaotic_block_gs", block_dims=(96, 1, 1), steps=2,
+                            strategy=ps.ExecutionStrategy.device(gs_mode="wavefront"))
+    _, hist = ps.smooth(g, cfg, ps.InverseCache())
+    for po, pg in zip(o.patches, g.patches):
+        assert G.rel_maxnorm(pg.u.cpu().numpy(), po.u) < TOL
+    assert G.hist_rel(hist, want) < TOL
+
+
+def test_chaotic_gs_factor_general_line_length():
+    o, g = _pair([((96, 48, 40), (0, 0, 0))], seed=21)
     want, hist = _run(o, g, steps=4, mode="chaotic")
     for s in range(1, len(want)):
         got_f, ref_f = hist[s] / hist[s - 1], want[s] / want[s - 1]
