@@ -969,7 +969,7 @@ int psm_halo_signal(int* flag_a, int* flag_b, int value, void* stream) {
 }
 
 int psm_halo_wait(const int* flags, int n, int value, void* stream) {
-  if (!flags || n < 1 || n > 8) return fail(PSM_EINVAL, "bad flag list");
+  if (!flags || n < 1 || n > 4096) return fail(PSM_EINVAL, "bad flag list");
   CUDA_TRY(launch_halo_wait(flags, n, value, (cudaStream_t)stream));
   return PSM_OK;
 }

@@ -443,9 +443,14 @@ class PatchLevelDomain:
     ``level`` a Level of the owned patches with the interface copies among
     them; ``sends`` / ``recvs`` the cross-rank copies touching this rank."""
 
-    def __init__(self, specs, rank, world, device=None, group=None, assignment="greedy"):
+    def __init__(self, specs, rank, world, device=None, group=None, assignment="greedy", halo="nccl"):
         from .grid import _abutments
         from .runtime import partition_patches
+
+        if halo not in ("nccl", "p2p"):
+            raise ValueError(f"halo must be 'nccl' or 'p2p', got {halo!r}")
+        self.halo = halo
+        self._peer = None  # _PeerLevelHalo, built on the first p2p run
 
         self.specs = [_PatchSpec(d, o) for d, o in specs]
         self.rank, self.world, self.group = rank, world, group
@@ -508,6 +513,132 @@ class PatchLevelDomain:
         return [(off[g], self.specs[g].dims.nz) for g in self.mine], acc
 
 
+_NO_PEER = 2**31 - 1  # flag value of ranks that never signal this one
+
+
+class _PeerLevelHalo:
+    """Cross-rank interface copies over peer memory for a PatchLevelDomain.
+
+    Every rank maps the buffers of the remote patches it copies from (CUDA
+    IPC) and runs those copies itself, as ordinary interface copies of a
+    ghost-only device plan whose patch table holds its own patches followed by
+    the mapped remote ones: one launch pulls every cross-rank face straight
+    out of the neighbours' memory, no pack, send, receive or unpack.
+
+    Two step flags per rank pair keep the buffers consistent (values only
+    grow; e is the epoch of earlier runs):
+      ready[q] = e+s+1  producer q swept step s (its new buffer is final)
+      read[q]  = e+s+1  consumer q pulled its step-s faces from this rank
+    A rank waits ready >= e+s+1 from its producers before pulling, and before
+    sweeping step s read >= e+s-1 from its consumers under Jacobi (that sweep
+    overwrites the buffer they pulled at step s-2) or read >= e+s under GS
+    (in place: the buffer they pulled at step s-1)."""
+
+    def __init__(self, domain, stencil):
+        lib = _lib.load()
+        dev = domain.patches[0].device
+        world, rank = domain.world, domain.rank
+        self.producers = sorted({domain.owner[c.src] for c in domain.recvs})
+        self.consumers = sorted({domain.owner[c.dst] for c in domain.sends})
+        self.ready = torch.empty(world, dtype=torch.int32, device=dev)
+        self.read = torch.empty(world, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=domain.group)
+        init_ready = [0 if q in self.producers else _NO_PEER for q in range(world)]
+        init_read = [0 if q in self.consumers else _NO_PEER for q in range(world)]
+        self.ready.copy_(torch.tensor(init_ready, dtype=torch.int32))
+        self.read.copy_(torch.tensor(init_read, dtype=torch.int32))
+        torch.cuda.synchronize(dev)
+        try:
+            mine = {"patches": {g: [_ipc_export(b) for b in domain.patches[i]._bufs]
+                                for i, g in enumerate(domain.mine)},
+                    "ready": _ipc_export(self.ready), "read": _ipc_export(self.read)}
+        except (_lib.LibraryError, ValueError) as e:
+            mine = {"error": str(e)}
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, mine, group=domain.group)
+        bad = [f"rank {r}: {i['error']}" for r, i in enumerate(allinfo) if "error" in i]
+        if bad:
+            raise _lib.LibraryError("peer interface copies: cannot export buffers (" + "; ".join(bad) + ")")
+        err = ""
+        try:
+            # remote source patches, in global order, after the local ones
+            remote = sorted({c.src for c in domain.recvs})
+            ridx = {g: len(domain.mine) + i for i, g in enumerate(remote)}
+            descs = [p._desc() for p in domain.patches]
+            self._remote_ptrs = []
+            for g in remote:
+                b0, b1 = (_ipc_import(h, off) for h, off in allinfo[domain.owner[g]]["patches"][g])
+                d = _lib.PatchDesc()
+                d.buf[0], d.buf[1], d.f = b0, b1, b0  # f is not read by interface copies
+                d.nx, d.ny, d.nz = domain.specs[g].dims.shape
+                descs.append(d)
+                self._remote_ptrs.append((b0, b1))
+            copies = []
+            for c in domain.recvs:
+                cd = _lib.CopyDesc()
+                cd.src, cd.dst = ridx[c.src], domain.local_index[c.dst]
+                for a in range(3):
+                    cd.src_lo[a], cd.dst_lo[a], cd.extent[a] = c.src_lo[a], c.dst_lo[a], c.extent[a]
+                copies.append(cd)
+            self.nall = len(descs)
+            pd = (_lib.PatchDesc * self.nall)(*descs)
+            cda = (_lib.CopyDesc * max(1, len(copies)))(*copies)
+            st = stencil._cstruct()
+            handle = ctypes.c_void_p()
+            _lib.check(lib.psm_plan_create(pd, self.nall, cda, len(copies), ctypes.byref(st), 0, None,
+                                           ctypes.byref(handle)), "psm_plan_create (peer copies)")
+            self.plan = handle.value
+            # the flag words this rank writes in each neighbour
+            self.ready_out = [_ipc_import(*allinfo[q]["ready"]) + 4 * rank for q in self.consumers]
+            self.read_out = [_ipc_import(*allinfo[q]["read"]) + 4 * rank for q in self.producers]
+        except (_lib.LibraryError, ValueError) as e:
+            err = str(e)
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=domain.group)
+        if any(errs):
+            raise _lib.LibraryError("peer interface copies unavailable: " + "; ".join(
+                f"rank {r}: {e}" for r, e in enumerate(errs) if e))
+        self.epoch = 0
+        self.world = world
+
+    def __del__(self):
+        h = getattr(self, "plan", None)
+        if h:
+            try:
+                _lib.load().psm_plan_destroy(h)
+            except Exception:
+                pass
+
+    def _signal(self, ptrs, value, stream):
+        lib = _lib.load()
+        for i in range(0, len(ptrs), 2):
+            a = ptrs[i]
+            b = ptrs[i + 1] if i + 1 < len(ptrs) else None
+            _lib.check(lib.psm_halo_signal(ctypes.c_void_p(a), ctypes.c_void_p(b), int(value), stream),
+                       "halo_signal")
+
+    def _wait(self, flags, value, stream):
+        _lib.check(_lib.load().psm_halo_wait(ctypes.c_void_p(flags.data_ptr()), self.world, int(value), stream),
+                   "halo_wait")
+
+    def before_sweep(self, s, in_place, stream):
+        lag = 0 if in_place else 1
+        if s >= 1 + lag and self.consumers:
+            self._wait(self.read, self.epoch + s - lag, stream)
+
+    def after_sweep(self, s, active, stream):
+        """The step's sweep, swap and local refresh are queued: publish, pull
+        the remote faces into this rank's ghosts, acknowledge."""
+        self._signal(self.ready_out, self.epoch + s + 1, stream)
+        if self.producers:
+            self._wait(self.ready, self.epoch + s + 1, stream)
+            act = (ctypes.c_ubyte * self.nall)(*([active] * self.nall))
+            _lib.check(_lib.load().psm_refresh_ghosts(self.plan, act, _lib.GHOST_INTERFACE, stream),
+                       "peer interface copies")
+        self._signal(self.read_out, self.epoch + s + 1, stream)
+
+
 def dist_smooth_level(domain, config, cache):
     """``smooth`` on a multi-patch level split over ranks by patch: every rank
     calls it with its own ``PatchLevelDomain``; returns the global history on
@@ -522,13 +653,27 @@ def dist_smooth_level(domain, config, cache):
     steps = config.steps
     jac = config.scheme == "block_jacobi"
     with torch.cuda.device(plan.device):
+        peer = None
+        if domain.halo == "p2p" and domain.world > 1:
+            try:  # collective; raises on every rank alike
+                if domain._peer is None:
+                    domain._peer = _PeerLevelHalo(domain, config.stencil)
+                peer = domain._peer
+            except _lib.LibraryError:
+                peer = None  # NCCL exchange
+        stream = ctypes.c_void_p(torch.cuda.current_stream(plan.device).cuda_stream)
         dp.reserve(steps + 1)
         dp.refresh(_lib.GHOST_ALL)
         domain.exchange()
+        if peer is not None:
+            torch.cuda.synchronize(plan.device)
+            dist.barrier(group=domain.group)
         if not jac:
             dp.residual(0)
         mode = _gs_mode(config)
         for s in range(steps):
+            if peer is not None:
+                peer.before_sweep(s, not jac, stream)
             if jac:
                 dp.jacobi(config.omega, s)
                 for p in level.patches:
@@ -537,9 +682,14 @@ def dist_smooth_level(domain, config, cache):
             else:
                 dp.gs(config.omega, mode)
                 dp.refresh(_lib.GHOST_ALL)
-            domain.exchange()
+            if peer is not None:
+                peer.after_sweep(s, level.patches[0]._active, stream)
+            else:
+                domain.exchange()
             if not jac:
                 dp.residual(s + 1)
+        if peer is not None:
+            peer.epoch += steps
         if jac:
             dp.residual(steps)
         slots, total = domain.plane_slots()

@@ -206,3 +206,13 @@ def test_gather_plane_sums_ragged_slabs(tmp_path):
     want = np.arange(17, dtype=np.float64)[None, :] + 100.0 * np.arange(2)[:, None]
     for r in range(world):
         np.testing.assert_array_equal(np.load(tmp_path / f"g{r}.npy"), want)
+
+
+def test_patch_level_domain_halo_modes():
+    from paper_1208_1975_b200.dist import PatchLevelDomain
+
+    specs = [((8, 4, 4), (0, 0, 0)), ((8, 4, 4), (8, 0, 0))]
+    d = PatchLevelDomain(specs, 0, 2, device="cpu", halo="p2p")
+    assert d.halo == "p2p" and d._peer is None
+    with pytest.raises(ValueError):
+        PatchLevelDomain(specs, 0, 2, device="cpu", halo="ucx")

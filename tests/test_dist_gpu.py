@@ -106,7 +106,7 @@ def _lattice_inputs():
     return [rng.standard_normal(PSIZE) for _ in range(n)], [rng.standard_normal(PSIZE) for _ in range(n)]
 
 
-def _level_rank_main(rank, world, port, out_dir, scheme, block):
+def _level_rank_main(rank, world, port, out_dir, scheme, block, halo="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -115,7 +115,7 @@ def _level_rank_main(rank, world, port, out_dir, scheme, block):
         from paper_1208_1975_b200.dist import PatchLevelDomain, dist_smooth_level
 
         torch.cuda.set_device(0)
-        dom = PatchLevelDomain(_lattice_specs(), rank, world, device="cuda:0")
+        dom = PatchLevelDomain(_lattice_specs(), rank, world, device="cuda:0", halo=halo)
         u0, f = _lattice_inputs()
         for g, p in zip(dom.mine, dom.patches):
             p.interior[...] = torch.from_numpy(u0[g]).cuda()
@@ -130,16 +130,21 @@ def _level_rank_main(rank, world, port, out_dir, scheme, block):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scheme,block", [("block_jacobi", (64, 1, 1)), ("chaotic_block_gs", (64, 1, 1)),
-                                          ("block_jacobi", (4, 4, 2)), ("chaotic_block_gs", (64, 8, 1))])
-def test_two_rank_patch_partition_matches_single_process(tmp_path, scheme, block):
+@pytest.mark.parametrize("scheme,block,halo", [("block_jacobi", (64, 1, 1), "nccl"),
+                                               ("chaotic_block_gs", (64, 1, 1), "nccl"),
+                                               ("block_jacobi", (4, 4, 2), "nccl"),
+                                               ("chaotic_block_gs", (64, 8, 1), "nccl"),
+                                               ("block_jacobi", (64, 1, 1), "p2p"),
+                                               ("chaotic_block_gs", (64, 8, 1), "p2p")])
+def test_two_rank_patch_partition_matches_single_process(tmp_path, scheme, block, halo):
     """C4-style lattice split by patch over 2 ranks (cross-rank interface
     copies packed/sent/unpacked): bitwise equal to the single-process level,
     iterates (ghosts included) and history."""
     import paper_1208_1975_b200 as ps
 
     world = 2
-    mp.spawn(_level_rank_main, args=(world, _free_port(), str(tmp_path), scheme, block), nprocs=world, join=True)
+    mp.spawn(_level_rank_main, args=(world, _free_port(), str(tmp_path), scheme, block, halo), nprocs=world,
+             join=True)
     u0, f = _lattice_inputs()
     patches = [ps.Patch(ps.PatchDims(*d), o) for d, o in _lattice_specs()]
     for p, a, b in zip(patches, u0, f):
@@ -249,7 +254,7 @@ def _mixed_inputs():
     return [rng.standard_normal(d) for d, _ in MIXED_SPECS], [rng.standard_normal(d) for d, _ in MIXED_SPECS]
 
 
-def _mixed_rank_main(rank, world, port, out_dir, scheme, block):
+def _mixed_rank_main(rank, world, port, out_dir, scheme, block, halo="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -258,13 +263,18 @@ def _mixed_rank_main(rank, world, port, out_dir, scheme, block):
         from paper_1208_1975_b200.dist import PatchLevelDomain, dist_smooth_level
 
         torch.cuda.set_device(0)
-        dom = PatchLevelDomain(MIXED_SPECS, rank, world, device="cuda:0")
+        dom = PatchLevelDomain(MIXED_SPECS, rank, world, device="cuda:0", halo=halo)
         u0, f = _mixed_inputs()
         for g, p in zip(dom.mine, dom.patches):
             p.interior[...] = torch.from_numpy(u0[g]).cuda()
             p.f[...] = torch.from_numpy(f[g]).cuda()
         cfg = ps.SmootherConfig(scheme=scheme, block_dims=block, steps=STEPS)
-        hist = dist_smooth_level(dom, cfg, ps.InverseCache())
+        cache = ps.InverseCache()
+        hist = dist_smooth_level(dom, cfg, cache)
+        if halo == "p2p":  # the peer path really ran, and a second call continues the flag epochs
+            assert dom._peer is not None and dom._peer.epoch == STEPS
+            hist2 = dist_smooth_level(dom, cfg, cache)
+            np.save(os.path.join(out_dir, f"mhist2_{rank}.npy"), np.array(hist2))
         for g, p in zip(dom.mine, dom.patches):
             np.save(os.path.join(out_dir, f"patch{g}.npy"), p.u.cpu().numpy())
         np.save(os.path.join(out_dir, f"mhist{rank}.npy"), np.array(hist))
@@ -273,16 +283,25 @@ def _mixed_rank_main(rank, world, port, out_dir, scheme, block):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scheme,block", [("block_jacobi", (32, 1, 1)), ("chaotic_block_gs", (32, 1, 1)),
-                                          ("block_jacobi", (4, 4, 4))])
-def test_mixed_patch_set_across_three_ranks(tmp_path, scheme, block):
+@pytest.mark.parametrize("scheme,block,halo", [("block_jacobi", (32, 1, 1), "nccl"),
+                                               ("chaotic_block_gs", (32, 1, 1), "nccl"),
+                                               ("block_jacobi", (4, 4, 4), "nccl"),
+                                               ("block_jacobi", (32, 1, 1), "p2p"),
+                                               ("chaotic_block_gs", (32, 1, 1), "p2p"),
+                                               ("block_jacobi", (4, 4, 4), "p2p"),
+                                               ("block_jacobi", (32, 32, 1), "p2p")])
+def test_mixed_patch_set_across_three_ranks(tmp_path, scheme, block, halo):
     """Seven patches of different sizes (partial-face abutment on every axis,
     some faces physical, some shared with two patches) split greedily over 3
-    ranks: bitwise equal to the single-process level, ghosts and history."""
+    ranks: bitwise equal to the single-process level, ghosts and history.
+    halo='p2p': the cross-rank faces are pulled from the neighbours' memory
+    (CUDA IPC) by one copy launch per step, step flags instead of NCCL; two
+    consecutive calls."""
     import paper_1208_1975_b200 as ps
 
     world = 3
-    mp.spawn(_mixed_rank_main, args=(world, _free_port(), str(tmp_path), scheme, block), nprocs=world, join=True)
+    mp.spawn(_mixed_rank_main, args=(world, _free_port(), str(tmp_path), scheme, block, halo), nprocs=world,
+             join=True)
     u0, f = _mixed_inputs()
     patches = [ps.Patch(ps.PatchDims(*d), o) for d, o in MIXED_SPECS]
     for p, a, b in zip(patches, u0, f):
@@ -291,8 +310,13 @@ def test_mixed_patch_set_across_three_ranks(tmp_path, scheme, block):
     lv = ps.Level(patches)
     assert len(lv.adjacency) >= len(MIXED_SPECS)  # the layout really has shared (partial) faces
     cfg = ps.SmootherConfig(scheme=scheme, block_dims=block, steps=STEPS)
-    _, want_hist = ps.smooth(lv, cfg, ps.InverseCache())
+    cache = ps.InverseCache()
+    _, want_hist = ps.smooth(lv, cfg, cache)
+    if halo == "p2p":
+        _, want_hist2 = ps.smooth(lv, cfg, cache)
     for g, p in enumerate(patches):
         np.testing.assert_array_equal(np.load(tmp_path / f"patch{g}.npy"), p.u.cpu().numpy())
     for r in range(world):
         np.testing.assert_array_equal(np.load(tmp_path / f"mhist{r}.npy"), np.array(want_hist))
+        if halo == "p2p":
+            np.testing.assert_array_equal(np.load(tmp_path / f"mhist2_{r}.npy"), np.array(want_hist2))
