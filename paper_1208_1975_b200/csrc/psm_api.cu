@@ -582,7 +582,11 @@ int psm_refresh_ghosts(psm_plan* P, const unsigned char* active, int what, void*
   int rc = get_active(P, active, &da);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (what & PSM_GHOST_PHYSICAL) {
+  // line-Jacobi sweeps of the one-tile and generic kernels write every
+  // physical ghost of v themselves
+  const bool swept = (what & PSM_GHOST_SKIP_X) && P->kind == PSM_BLOCK_LINE && !P->phys_pending;
+  if (what & PSM_GHOST_PHYSICAL) P->phys_pending = 0;
+  if ((what & PSM_GHOST_PHYSICAL) && !swept) {
     CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->ghost_max_face,
                                     (what & PSM_GHOST_SKIP_X) ? 1 : 0, s));
     P->launches += P->ghost_total > 0;
@@ -735,6 +739,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms,
                                    P->fac[p]->h_line, s, nullptr, peers ? 1 : 0));
+      P->phys_pending = 1;  // y/z ghosts left to the refresh
       P->launches += 1;
     } else if (zgen_ok(P, p) && zgen_cells(P, p, pb, ka, kb, &q) >= zmin) {
       // other even nx: the z-marching pipeline with the line length per unit,
@@ -750,6 +755,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       for (int r = p; r < q; ++r) nxs.push_back(P->hp[r].nx);
       CUDA_TRY(launch_line_zgen(nxs.data(), (int)nxs.size(), unit ? 1 : 0, P->d_patches, da, P->st, omega, part,
                                 units, nu, sms, P->fac[p]->h_line, s));
+      P->phys_pending = 1;
       P->launches += 1;
     } else if (ka == 0 && kb < 0) {
       // whole-patch sweeps of consecutive patches the specialised kernels do

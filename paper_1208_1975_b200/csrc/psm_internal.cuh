@@ -136,6 +136,39 @@ __device__ __forceinline__ double relax(double u, double omega, double x) {
 
 constexpr int kMaxTileCells = 2048;  // cells per line tile (8 per thread at 256 threads)
 
+// Physical ghosts of v fused into a line-Jacobi sweep (grid.py:311-330 in the
+// closed form of physical_ghost_kernel): the cell (x, j, k) just written with
+// value nv (v index iu) also fills every y/z ghost cell whose nearest interior
+// cell it is, sign (-1)^(number of ghost coordinates).  The x-only ghosts are
+// the caller's (it already writes them).  The interior of a z face flagged as
+// a peer interface (PatchDev::iface) is left to the neighbour's stores; its
+// edges are still filled.  Call only for cells on a y or z boundary.
+__device__ __forceinline__ void fused_yz_ghosts(double* __restrict__ v, long long iu, double nv, int x, int j, int k,
+                                                int nx, int ny, int nz, long long px, long long pxy, int iface) {
+  const int xs[3] = {0, x == 0 ? -1 : 2, x == nx - 1 ? 1 : 2};
+  const int ys[3] = {0, j == 0 ? -1 : 2, j == ny - 1 ? 1 : 2};
+  const int zs[3] = {0, k == 0 ? -1 : 2, k == nz - 1 ? 1 : 2};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int sz = zs[c];
+    if (sz == 2) continue;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const int sy = ys[b];
+      if (sy == 2) continue;
+      if (sy == 0 && sz == 0) continue;  // x-only ghosts: the caller's
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int sx = xs[a];
+        if (sx == 2) continue;
+        if (sx == 0 && sy == 0 && ((sz < 0 && (iface & 1)) || (sz > 0 && (iface & 2)))) continue;
+        const int flips = (sx != 0) + (sy != 0) + (sz != 0);
+        v[iu + sx + sy * px + sz * pxy] = (flips & 1) ? -nv : nv;
+      }
+    }
+  }
+}
+
 }  // namespace psm
 
 #include <map>
@@ -197,6 +230,10 @@ struct psm_plan {
   GsPipeState* gspipe = nullptr;
   int* d_gsflags = nullptr;  // nplanes progress words + one ticket per group
   int gs_ntickets = 0;
+  // a line-Jacobi kernel that leaves the y/z physical ghosts of v to the
+  // refresh (z-marching kernels) ran since the last ghost refresh; the
+  // one-tile and generic kernels write them in their epilogue
+  int phys_pending = 1;
   // box path: blocks (patch, x0, y0, z0) sorted by wavefront bi+bj+bk (GS),
   // and Jacobi regions of (8/bx) x (8/by) x (8/bz) blocks
   int4* d_boxes = nullptr;

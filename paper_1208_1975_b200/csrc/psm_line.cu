@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __res
 
   // ---- C: interfaces, spike correction, relaxation, store ----------------
   const double up = L->up, up_h31 = L->up_h31;
+  const bool yz_edge = j0 == 0 || j0 + R >= ny || k == 0 || k == P.nz - 1;  // tile touches a y/z face
 #pragma unroll
   for (int h = 0; h < kMaxE; ++h) {
     const int e = h * T + tid;
@@ -166,6 +167,11 @@ __global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __res
       v[iu] = nv;
       if (x == 0) v[iu - 1] = -nv;
       if (x == nx - 1) v[iu + 1] = -nv;
+      if (yz_edge) {
+        const int j = j0 + r;
+        if (j == 0 || j == ny - 1 || k == 0 || k == P.nz - 1)
+          fused_yz_ghosts(v, iu, nv, x, j, k, nx, ny, P.nz, px, pxy, P.iface);
+      }
     }
   }
 }
@@ -214,6 +220,8 @@ __global__ void line_generic_jacobi_kernel(const PatchDev* __restrict__ patches,
   }
   v[ub - 1] = -v[ub];
   v[ub + nx] = -v[ub + nx - 1];
+  if (j == 0 || j == ny - 1 || k == 0 || k == P.nz - 1)
+    for (int x = 0; x < nx; ++x) fused_yz_ghosts(v, ub + x, v[ub + x], x, j, k, nx, ny, P.nz, px, pxy, P.iface);
 }
 
 // Apply the exact line inverse to `count` contiguous vectors of length nx
@@ -398,6 +406,7 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
     __syncthreads();  // (2) y, cl, cr complete
 
     // ---- C ----------------------------------------------------------------
+    const bool yz_edge = j0 == 0 || j0 + rows >= ny || k == 0 || k == P.nz - 1;  // tile touches a y/z face
 #pragma unroll
     for (int h = 0; h < E; ++h) {
       const int e = h * T + tid;
@@ -411,6 +420,11 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
         v[iu] = nv;
         if (x == 0) v[iu - 1] = -nv;
         if (x == NX - 1) v[iu + 1] = -nv;
+        if (yz_edge) {
+          const int j = j0 + row;
+          if (j == 0 || j == ny - 1 || k == 0 || k == P.nz - 1)
+            fused_yz_ghosts(v, iu, nv, x, j, k, NX, ny, P.nz, PX, pxy, P.iface);
+        }
       }
     }
   }
