@@ -101,9 +101,11 @@ int psm_plan_reserve_history(psm_plan* plan, int slots);
  * (grid.py:523-547).  active[p] selects the buffer holding u for patch p.
  * `what` ORs psm_ghost_part bits: PSM_GHOST_PHYSICAL alone is
  * fill_physical_ghosts, PSM_GHOST_INTERFACE alone exchange_interface_ghosts;
- * PSM_GHOST_SKIP_X leaves to the preceding Jacobi sweep the physical faces it
- * already wrote in its epilogue: the x faces for every block kind, all faces
- * (edges and corners included) for line plans. */
+ * PSM_GHOST_SKIP_X (right after a sweep) fills only the physical ghosts that
+ * sweep's epilogue left: none after the one-tile / generic line-Jacobi
+ * kernels, the y/z faces after the z-marching line-Jacobi, plane and box
+ * Jacobi sweeps (their epilogues write the x faces), all after GS sweeps.
+ * The plan tracks which. */
 enum psm_ghost_part { PSM_GHOST_PHYSICAL = 1, PSM_GHOST_INTERFACE = 2, PSM_GHOST_SKIP_X = 4, PSM_GHOST_ALL = 3 };
 int psm_refresh_ghosts(psm_plan* plan, const unsigned char* active, int what, void* stream);
 

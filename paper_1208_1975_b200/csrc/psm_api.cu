@@ -582,14 +582,15 @@ int psm_refresh_ghosts(psm_plan* P, const unsigned char* active, int what, void*
   int rc = get_active(P, active, &da);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  // line-Jacobi sweeps of the one-tile and generic kernels write every
-  // physical ghost of v themselves
-  const bool swept = (what & PSM_GHOST_SKIP_X) && P->kind == PSM_BLOCK_LINE && !P->phys_pending;
-  if (what & PSM_GHOST_PHYSICAL) P->phys_pending = 0;
-  if ((what & PSM_GHOST_PHYSICAL) && !swept) {
-    CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->ghost_max_face,
-                                    (what & PSM_GHOST_SKIP_X) ? 1 : 0, s));
-    P->launches += P->ghost_total > 0;
+  // after a sweep (SKIP_X) only what its epilogue left: nothing, the y/z
+  // faces plus the x-face perimeters, or everything
+  const int level = (what & PSM_GHOST_SKIP_X) ? P->phys_pending : 2;
+  if (what & PSM_GHOST_PHYSICAL) {
+    if (level > 0) {
+      CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->ghost_max_face, level == 1 ? 1 : 0, s));
+      P->launches += P->ghost_total > 0;
+    }
+    P->phys_pending = 0;
   }
   if (what & PSM_GHOST_INTERFACE) {
     CUDA_TRY(launch_interface_copies(P->d_patches, da, P->d_copies, P->ncopy, P->copy_max, s));
@@ -739,7 +740,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       CUDA_TRY(launch_line_zmarch(nx, unit ? 1 : 0, P->d_patches, da, P->st, omega, part, units, nu, sms,
                                    P->fac[p]->h_line, s, nullptr, peers ? 1 : 0));
-      P->phys_pending = 1;  // y/z ghosts left to the refresh
+      P->phys_pending = std::max(P->phys_pending, 1);  // y/z ghosts left to the refresh
       P->launches += 1;
     } else if (zgen_ok(P, p) && zgen_cells(P, p, pb, ka, kb, &q) >= zmin) {
       // other even nx: the z-marching pipeline with the line length per unit,
@@ -755,7 +756,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
       for (int r = p; r < q; ++r) nxs.push_back(P->hp[r].nx);
       CUDA_TRY(launch_line_zgen(nxs.data(), (int)nxs.size(), unit ? 1 : 0, P->d_patches, da, P->st, omega, part,
                                 units, nu, sms, P->fac[p]->h_line, s));
-      P->phys_pending = 1;
+      P->phys_pending = std::max(P->phys_pending, 1);
       P->launches += 1;
     } else if (ka == 0 && kb < 0) {
       // whole-patch sweeps of consecutive patches the specialised kernels do
@@ -838,6 +839,7 @@ int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (P->kind == PSM_BLOCK_LINE) return sweep_planes(P, da, omega, part, 0, P->npatch, 0, -1, s);
+  if (P->kind != 0) P->phys_pending = std::max(P->phys_pending, 1);  // plane/box sweeps write x faces only
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_jacobi(P, da, omega, part, s);
   if (P->kind == PSM_BLOCK_BOX) {
     if (slot >= 0) {  // history entry of the current iterate (tile partials)
@@ -1011,7 +1013,7 @@ static int smooth_sequence(psm_plan* P, std::vector<unsigned char>& act, int sch
   for (int s = 0; s < steps; ++s) {
     rc = psm_gs_sweep(P, act.data(), omega, gs_mode, stream);
     if (rc) return rc;
-    rc = psm_refresh_ghosts(P, act.data(), PSM_GHOST_ALL, stream);
+    rc = psm_refresh_ghosts(P, act.data(), PSM_GHOST_ALL | PSM_GHOST_SKIP_X, stream);
     if (rc) return rc;
     if (history) {
       rc = psm_residual(P, act.data(), s + 1, stream);
@@ -1120,6 +1122,7 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
   int rc = get_active(P, active, &da);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  P->phys_pending = 2;  // GS sweeps leave every physical ghost to the refresh
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_gs(P, da, omega, s);
   if (P->kind == PSM_BLOCK_BOX) {  // lexicographic block order = wavefronts bi+bj+bk, in place
     for (size_t w = 0; w + 1 < P->box_wave_off.size(); ++w) {

@@ -230,10 +230,11 @@ struct psm_plan {
   GsPipeState* gspipe = nullptr;
   int* d_gsflags = nullptr;  // nplanes progress words + one ticket per group
   int gs_ntickets = 0;
-  // a line-Jacobi kernel that leaves the y/z physical ghosts of v to the
-  // refresh (z-marching kernels) ran since the last ghost refresh; the
-  // one-tile and generic kernels write them in their epilogue
-  int phys_pending = 1;
+  // physical ghosts the sweeps since the last refresh left to it: 0 none
+  // (one-tile / generic line-Jacobi kernels: written in their epilogues), 1
+  // the y/z faces (z-marching line Jacobi, plane and box Jacobi: x faces
+  // written), 2 all (GS sweeps); consulted by a refresh with PSM_GHOST_SKIP_X
+  int phys_pending = 2;
   // box path: blocks (patch, x0, y0, z0) sorted by wavefront bi+bj+bk (GS),
   // and Jacobi regions of (8/bx) x (8/by) x (8/bz) blocks
   int4* d_boxes = nullptr;

@@ -343,7 +343,7 @@ def dist_smooth(domain, config, cache, record_history=True):
                     dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
                 else:
                     dp.gs(config.omega, mode)
-                    dp.refresh(_lib.GHOST_ALL)
+                    dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)  # what the sweep left
                 reqs = domain.start_exchange(domain.patch._active)
                 domain.finish_exchange(reqs)
                 domain.unpack(dp)
@@ -681,7 +681,7 @@ def dist_smooth_level(domain, config, cache):
                 dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
             else:
                 dp.gs(config.omega, mode)
-                dp.refresh(_lib.GHOST_ALL)
+                dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)  # what the sweep left
             if peer is not None:
                 peer.after_sweep(s, level.patches[0]._active, stream)
             else:

@@ -194,7 +194,7 @@ def _run(level, config, plan, steps, history, timers):
             for s in range(steps):
                 dp.gs(config.omega, mode)
                 with gt:
-                    dp.refresh(_lib.GHOST_ALL)
+                    dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)  # what the sweep left
                 if history:
                     dp.residual(s + 1)
         sums = dp.sumsq(steps + 1) if history else None
