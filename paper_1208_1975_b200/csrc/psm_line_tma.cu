@@ -68,6 +68,17 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// f is read once: its bulk copies carry an L2 evict-first policy, so the
+// u rows the neighbouring columns re-read as y-halos stay resident longer
+__device__ __forceinline__ void tma_load_1d_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -175,7 +186,11 @@ struct ZAC {
         if (FULL || row < rows) {
           const double nv = relax(cold[p * RPT + r], omega, xb[row * RS + x + (x >> 5)]);
           const long long iu = vbase_old + (long long)row * PX + x;
+#ifdef PSM_ZMARCH_NO_HINT
           v[iu] = nv;
+#else
+          __stcs(v + iu, nv);  // streaming store: v is not re-read by this sweep
+#endif
           if constexpr (NX_GE) {
             if (p == 0 && tid == 0) v[iu - 1] = -nv;
             if (p == NXP - 1 && tid == ACT - 1) v[iu + 1] = -nv;
@@ -375,7 +390,11 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
           const int t = nf % C::NF;
           mbar_wait(&empty_f[t], ((nf / C::NF) & 1) ^ 1);
           mbar_expect_tx(&full_f[t], fbytes);
+#ifdef PSM_ZMARCH_NO_HINT
           tma_load_1d(fring + t * C::FS, P.f + ((long long)kf * P.ny + U.j0) * NX, fbytes, &full_f[t]);
+#else
+          tma_load_1d_evict_first(fring + t * C::FS, P.f + ((long long)kf * P.ny + U.j0) * NX, fbytes, &full_f[t]);
+#endif
           ++nf;
         }
       }
