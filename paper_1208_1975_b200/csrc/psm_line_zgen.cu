@@ -359,11 +359,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         double* seg = rbuf + b * sb + r * G.rs + s * (kSeg + 1);
         double yfirst = 0.0, ylast = 0.0;
-#ifdef PSM_ZGEN_NOSOLVE
-        if (false) {
-#else
         if (live) {
-#endif
           double y[kSeg];
 #pragma unroll
           for (int i = 0; i < kSeg; ++i) y[i] = i < len ? seg[i] * T.invm[i] : 0.0;
@@ -382,11 +378,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         const double yl_left = __shfl_up_sync(0xffffffffu, ylast, 1);
         const double yf_right = __shfl_down_sync(0xffffffffu, yfirst, 1);
-#ifdef PSM_ZGEN_NOSOLVE
-        if (false) {
-#else
         if (live) {
-#endif
           double clv = 0.0, crv = 0.0;
           if (s > 0) clv = lo * ((yl_left - up_h31 * yfirst) * (last ? d_tail : T.d_full));
           if (!last) {
