@@ -412,6 +412,17 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     P->copy_max = std::max(P->copy_max, (long long)c.extent[0] * c.extent[1] * c.extent[2]);
   }
   P->copy_total = e0;
+  // faces one copy covers entirely: the physical fill skips their interior
+  for (int i = 0; i < ncopy; ++i) {
+    const psm_copy_desc& c = copies[i];
+    const int dd[3] = {patches[c.dst].nx, patches[c.dst].ny, patches[c.dst].nz};
+    for (int a = 0; a < 3; ++a) {
+      if (c.extent[a] != 1 || (c.dst_lo[a] != -1 && c.dst_lo[a] != dd[a])) continue;
+      const int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
+      if (c.dst_lo[b1] == 0 && c.extent[b1] == dd[b1] && c.dst_lo[b2] == 0 && c.extent[b2] == dd[b2])
+        P->hp[c.dst].covered |= 1 << (2 * a + (c.dst_lo[a] == -1 ? 0 : 1));
+    }
+  }
   cudaError_t err = cudaMalloc(&P->d_patches, npatch * sizeof(PatchDev));
   if (err == cudaSuccess) err = cudaMemcpy(P->d_patches, P->hp.data(), npatch * sizeof(PatchDev), cudaMemcpyHostToDevice);
   if (err == cudaSuccess) err = cudaMalloc(&P->d_gprefix, npatch * sizeof(long long));

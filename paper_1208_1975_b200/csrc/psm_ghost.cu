@@ -29,7 +29,9 @@ __global__ void __launch_bounds__(256) physical_ghost_kernel(const PatchDev* __r
   const int px = P.nx + 2, py = P.ny + 2, pz = P.nz + 2;
   // face extent (A fastest, then B)
   const int A = axis == 0 ? py : px, B = axis == 2 ? py : pz;
-  const bool perim = axis == 0 && skip_x;
+  // faces whose interior something else writes (the Jacobi sweep's x faces,
+  // a face one interface copy covers, a peer-halo z face): perimeter only
+  const bool perim = (axis == 0 && skip_x) || ((P.covered >> face) & 1) || (axis == 2 && ((P.iface >> side) & 1));
   const int n = perim ? 2 * A + 2 * (B - 2) : A * B;
   for (int c = blockIdx.x * 1024 + threadIdx.x; c < min(n, (int)(blockIdx.x + 1) * 1024); c += 256) {
     int a, b;
@@ -50,8 +52,6 @@ __global__ void __launch_bounds__(256) physical_ghost_kernel(const PatchDev* __r
     if (axis == 0) { i = side ? px - 1 : 0; j = a; k = b; }
     else if (axis == 1) { i = a; j = side ? py - 1 : 0; k = b; }
     else { i = a; j = b; k = side ? pz - 1 : 0; }
-    // the interior of an interface z face belongs to the neighbour's data
-    if (axis == 2 && (P.iface >> side & 1) && i > 0 && i < px - 1 && j > 0 && j < py - 1) continue;
     const int ic = min(max(i, 1), px - 2), jc = min(max(j, 1), py - 2), kc = min(max(k, 1), pz - 2);
     const int flips = (i != ic) + (j != jc) + (k != kc);
     const double val = u[(long long)ic + (long long)px * (jc + (long long)py * kc)];

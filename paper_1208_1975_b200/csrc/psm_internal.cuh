@@ -83,6 +83,9 @@ struct PatchDev {
   double* peer_hi[2];
   int peer_lo_nz;
   int iface;
+  // bit 2*axis+side: that face's interior is wholly rewritten by one interface
+  // copy, so the physical fill only needs its perimeter (edges, corners)
+  int covered;
 };
 
 struct CopyDev {
