@@ -48,7 +48,11 @@ namespace psm {
 constexpr int kGsW = 7;       // planes (compute warps) per CTA unit; + 1 publisher warp
 constexpr int kGsThreads = (kGsW + 1) * 32;
 constexpr int kGsTab = 18;    // per-lane table entries: q0,q1,q2 + 5 PCR steps x (p0,p1,p2)
-constexpr int kGsPub = 4;     // wavefront mode: rows per release of the cross-CTA flag
+#ifdef PSM_GS_PUB
+constexpr int kGsPub = PSM_GS_PUB;  // tuning builds
+#else
+constexpr int kGsPub = 2;     // wavefront mode: rows per release of the cross-CTA flag (1: 0.78, 2: 0.77, 4: 0.82 ms at C2)
+#endif
 
 // uniform chunk-interior tables (passed by value: constant-bank operands)
 struct GsUniform {
