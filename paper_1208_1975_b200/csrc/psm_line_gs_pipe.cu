@@ -65,11 +65,19 @@ template <int NC>
 struct GCfg {
   static constexpr int IS = 32 + 16 / NC;      // stride between the NC "i-rows" of a slot
   static constexpr int SLOT = (NC * IS + 3) / 2 * 2;  // doubles per ring slot (+ the two x-ghosts), even: 16-B bulk copies
+#ifdef PSM_GS_D
+  static constexpr int D = PSM_GS_D;           // tuning builds
+#else
   static constexpr int D = 3;                  // prefetch ring depth
+#endif
   static constexpr int P = D - 1;              // rows of prefetch ahead
   static constexpr int DH = 2;                 // new-row ring depth (warp -> next warp)
   static constexpr int DHL = 4;                // new-row ring depth (last warp -> publisher)
+#ifdef PSM_GS_DM
+  static constexpr int DM = PSM_GS_DM;         // tuning builds
+#else
   static constexpr int DM = 3;                 // warp 0: rows of plane k0-1 in flight (TMA)
+#endif
   static constexpr int MROW = 32 * NC + 2;     // padded row, contiguous
   static constexpr int NBAR = 2 * kGsW * DH + 2 * DHL + DM;  // mbarriers
   static constexpr int HEAD_DOUBLES = kGsTab * 32 + 8 + NBAR + (NBAR & 1);  // tables, ints, mbarriers
