@@ -116,6 +116,89 @@ __global__ void plane_modal_thomas_kernel(const PlaneFac* __restrict__ F, double
   }
 }
 
+// The same modal solves with two threads per line (symmetric y faces):
+// the top thread eliminates rows 0..m-1 downwards, the bottom thread rows
+// ny-1..m upwards with the same factors (for lo == up the elimination from
+// the bottom is the mirror image), the pair meets in an exact 2x2 system for
+// x(m-1), x(m) (values swapped by shuffle), and each back-substitutes
+// outwards: half the dependent chain of the one-thread sweep, exact.
+__global__ void plane_modal_thomas2_kernel(const PlaneFac* __restrict__ F, double* __restrict__ buf,
+                                           long long nplanes) {
+  constexpr int B = 16;
+  const int nx = F->nx, ny = F->ny, m = ny / 2;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool in = t < 2 * nplanes * nx;  // whole warps stay for the shuffles
+  const long long line = in ? t >> 1 : 0;
+  const int bot = (int)(t & 1);
+  const long long pl = line / nx;
+  const int i = (int)(line - pl * nx);
+  double* b = buf + pl * (long long)nx * ny + i;
+  const double* cp = F->cp + i;
+  const double* invm = F->invm + i;
+  const double lo = F->fy_lo;  // == fy_up
+  // this thread's rows: top j = jj, bottom j = ny-1-jj, jj = 0..len-1
+  const int len = bot ? ny - m : m;
+  const long long j0 = bot ? ny - 1 : 0, dj = bot ? -nx : nx;
+  double prev = 0.0;
+  int jj = 0;
+  if (in) {
+    for (; jj + B <= len; jj += B) {
+      double v[B], mm[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        v[q] = b[j0 * nx + (jj + q) * dj];
+        mm[q] = __ldg(invm + (long long)(jj + q) * nx);
+      }
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        prev = fma(-lo, prev, v[q]) * mm[q];
+        b[j0 * nx + (jj + q) * dj] = prev;
+      }
+    }
+    for (; jj < len; ++jj) {
+      prev = fma(-lo, prev, b[j0 * nx + jj * dj]) * invm[(long long)jj * nx];
+      b[j0 * nx + jj * dj] = prev;
+    }
+  }
+  // meet: top x(m-1) = yT - cT x(m), bottom x(m) = yB - cB x(m-1)
+  const double c_own = in && len > 0 ? __ldg(cp + (long long)(len - 1) * nx) : 0.0;
+  const double y_oth = __shfl_xor_sync(0xffffffffu, prev, 1);
+  const double c_oth = __shfl_xor_sync(0xffffffffu, c_own, 1);
+  const double yT = bot ? y_oth : prev, yB = bot ? prev : y_oth;
+  const double cT = bot ? c_oth : c_own, cB = bot ? c_own : c_oth;
+  const double xT = (yT - cT * yB) / (1.0 - cT * cB);
+  double next = bot ? yB - cB * xT : xT;
+  if (!in || len == 0) return;
+  b[j0 * nx + (len - 1) * dj] = next;
+  jj = len - 2;
+  for (; jj - B + 1 >= 0; jj -= B) {
+    double v[B], c[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      v[q] = b[j0 * nx + (jj - q) * dj];
+      c[q] = __ldg(cp + (long long)(jj - q) * nx);
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      next = fma(-c[q], next, v[q]);
+      b[j0 * nx + (jj - q) * dj] = next;
+    }
+  }
+  for (; jj >= 0; --jj) {
+    next = fma(-cp[(long long)jj * nx], next, b[j0 * nx + jj * dj]);
+    b[j0 * nx + jj * dj] = next;
+  }
+}
+
+static void launch_modal_thomas(const PlaneFac& h, const PlaneFac* d, double* buf, long long nplanes,
+                                cudaStream_t s) {
+  if (h.fy_lo == h.fy_up && h.ny >= 2 && !getenv("PSM_PLANE_THOMAS1")) {
+    plane_modal_thomas2_kernel<<<(unsigned)((2 * nplanes * h.nx + 127) / 128), 128, 0, s>>>(d, buf, nplanes);
+  } else {
+    plane_modal_thomas_kernel<<<(unsigned)((nplanes * h.nx + 127) / 128), 128, 0, s>>>(d, buf, nplanes);
+  }
+}
+
 // Jacobi epilogue: v = u + omega * x for every interior cell, plus the
 // physical x-face ghosts of v (fused, see psm_line.cu).
 __global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
@@ -197,6 +280,7 @@ using namespace psm;
 struct PlaneRun {  // consecutive patches sharing one PlaneFac (same nx, ny)
   int p0, p1;
   const PlaneFac* d_fac;
+  const PlaneFac* h_fac;
   const double* Q;
   int nx, ny;
   int bw = 0;              // banded factorised solve available (psm_plane_band.cu)
@@ -317,7 +401,7 @@ int psm_plane_apply(const psm_factors* F, const double* r, double* x, long long 
   cublasSetStream(h, stream);
   int rc = dst_gemm(h, H.Q, H.nx, r, tmp, (long long)H.ny * count);
   if (rc == PSM_OK) {
-    plane_modal_thomas_kernel<<<(unsigned)((count * H.nx + 127) / 128), 128, 0, stream>>>(F->d_plane, tmp, count);
+    launch_modal_thomas(H, F->d_plane, tmp, count, stream);
     rc = dst_gemm(h, H.Q, H.nx, tmp, x, (long long)H.ny * count);
   }
   cudaFreeAsync(tmp, stream);
@@ -355,6 +439,7 @@ int psm_plane_plan_setup(psm_plan* P) {
     r.p0 = p;
     r.p1 = q;
     r.d_fac = P->fac[p]->d_plane;
+    r.h_fac = &P->fac[p]->h_plane;
     r.Q = P->fac[p]->h_plane.Q;
     r.nx = P->hp[p].nx;
     r.ny = P->hp[p].ny;
@@ -423,7 +508,7 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
     const long long nvec = planes * r.ny;
     int rc = dst_gemm(S->handle, r.Q, r.nx, S->rbuf + c0, S->rhat + c0, nvec);
     if (rc) return rc;
-    plane_modal_thomas_kernel<<<(unsigned)((planes * r.nx + 127) / 128), 128, 0, s>>>(r.d_fac, S->rhat + c0, planes);
+    launch_modal_thomas(*r.h_fac, r.d_fac, S->rhat + c0, planes, s);
     PCUDA(cudaGetLastError());
     rc = dst_gemm(S->handle, r.Q, r.nx, S->rhat + c0, S->rbuf + c0, nvec);
     if (rc) return rc;
@@ -458,8 +543,7 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
         const long long nplanes = p1 - p0;
         int rc = dst_gemm(S->handle, r.Q, r.nx, S->sbuf + o, S->shat + o, nplanes * r.ny);
         if (rc) return rc;
-        plane_modal_thomas_kernel<<<(unsigned)((nplanes * r.nx + 127) / 128), 128, 0, s>>>(r.d_fac, S->shat + o,
-                                                                                           nplanes);
+        launch_modal_thomas(*r.h_fac, r.d_fac, S->shat + o, nplanes, s);
         PCUDA(cudaGetLastError());
         rc = dst_gemm(S->handle, r.Q, r.nx, S->shat + o, S->sbuf + o, nplanes * r.ny);
         if (rc) return rc;
