@@ -233,33 +233,28 @@ __global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npa
 // place, then r(k+1) = f - A u at the same (x, y), which reads u(k) only at
 // this cell (its z-neighbour, just updated by this thread) and plane k+1's
 // old values; r(k+1) overwrites x in the stage buffer (same element).
+// grid (cell blocks of the largest plane, patch): no patch search per cell
 __global__ void plane_stage_relax_residual_kernel(const PatchDev* __restrict__ patches, int npatch,
                                                   const unsigned char* __restrict__ active, StencilDev st,
                                                   double omega, int k, const long long* __restrict__ stage_off,
                                                   double* __restrict__ sbuf, long long total) {
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
-       g += (long long)gridDim.x * blockDim.x) {
-    int lo = 0, hi = npatch - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (stage_off[mid] <= g) lo = mid; else hi = mid - 1;
-    }
-    const PatchDev& P = patches[lo];
-    const long long e = g - stage_off[lo];
-    const int nx = P.nx, ny = P.ny;
-    if (e >= (long long)nx * ny) continue;
+  const int lo = blockIdx.y;
+  const PatchDev& P = patches[lo];
+  const int nx = P.nx, ny = P.ny;
+  if (k >= P.nz) return;  // this patch has no stage k (nothing to relax, no plane k+1)
+  const long long off = stage_off[lo];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)nx * ny;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long g = off + e;
     const int j = (int)(e / nx), x = (int)(e - (long long)j * nx);
     const long long px = nx + 2, pxy = px * (ny + 2);
     double* u = P.buf[active[lo]];
     const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
-    double un = 0.0;
-    if (k < P.nz) {
-      un = relax(u[iu], omega, sbuf[g]);
-      u[iu] = un;
-    }
+    const double un = relax(u[iu], omega, sbuf[g]);
+    u[iu] = un;
     if (k + 1 < P.nz) {
       const long long iv = iu + pxy;  // (x, j, k+1)
-      const double zm = (k < P.nz) ? un : u[iv - pxy];
+      const double zm = un;
       sbuf[g] = residual7(st, P.f[((long long)(k + 1) * ny + j) * nx + x], u[iv], u[iv - 1], u[iv + 1], u[iv - px],
                           u[iv + px], zm, u[iv + pxy]);
     }
@@ -300,6 +295,7 @@ struct PlaneState {
   double* shat = nullptr;
   long long* d_stage_off = nullptr;
   long long stage_total = 0;
+  long long stage_max = 0;  // cells of the largest patch plane
 
   std::vector<long long> stage_off;
   std::vector<PlaneRun> runs;
@@ -428,6 +424,8 @@ int psm_plane_plan_setup(psm_plan* P) {
     so += (long long)P->hp[p].nx * P->hp[p].ny;
   }
   S->stage_total = so;
+  for (int p = 0; p < P->npatch; ++p)
+    S->stage_max = std::max<long long>(S->stage_max, (long long)P->hp[p].nx * P->hp[p].ny);
   PCUDA(cudaMalloc(&S->sbuf, so * sizeof(double)));
   PCUDA(cudaMalloc(&S->shat, so * sizeof(double)));
   PCUDA(cudaMalloc(&S->d_stage_off, P->npatch * sizeof(long long)));
@@ -552,7 +550,7 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
       }
     }
     // relax stage k and form stage k+1's residual in one pass
-    plane_stage_relax_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(
+    plane_stage_relax_residual_kernel<<<dim3(blocks_for(S->stage_max, 256), P->npatch), 256, 0, s>>>(
         P->d_patches, P->npatch, da, P->st, omega, k, S->d_stage_off, S->sbuf, S->stage_total);
     PCUDA(cudaGetLastError());
     P->launches += 1;
