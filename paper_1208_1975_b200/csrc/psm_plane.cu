@@ -199,6 +199,112 @@ static void launch_modal_thomas(const PlaneFac& h, const PlaneFac* d, double* bu
   }
 }
 
+// Plane GS in the transformed domain, stage k (symmetric y faces).  With
+// rhat = Q r (DST-I along x; Q = Q^T = Q^-1) and the exact plane inverse
+// x = Q S(Q r) (S: the modal y-solves), stage k's residual is the pre-sweep
+// residual minus zm * omega * x(k-1) at the same (x, y), so
+//   rhat(k) = rhat_pre(k) - zm omega xhat(k-1),   xhat(k) = S(rhat(k)),
+// and no transform runs inside the stage loop: one DGEMM transforms every
+// plane's pre-sweep residual before it, one transforms every xhat back after
+// it.  Thread pair per (patch, mode) as plane_modal_thomas2_kernel; planes
+// of patches p0.. at their own offsets in `buf` (cell-major, cell0).
+__global__ void plane_gs_stage_kernel(const PlaneFac* __restrict__ F, const PatchDev* __restrict__ patches, int p0,
+                                      long long nplanes, int k, double czw, double* __restrict__ buf) {
+  constexpr int B = 16;
+  const int nx = F->nx, ny = F->ny, m = ny / 2;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool in = t < 2 * nplanes * nx;
+  const long long line = in ? t >> 1 : 0;
+  const int bot = (int)(t & 1);
+  const long long pl = line / nx;
+  const int i = (int)(line - pl * nx);
+  const long long plane_cells = (long long)nx * ny;
+  double* b = buf + patches[p0 + pl].cell0 + (long long)k * plane_cells + i;
+  const double* bp = b - plane_cells;  // xhat(k-1) of the same patch (k > 0)
+  const double* cp = F->cp + i;
+  const double* invm = F->invm + i;
+  const double lo = F->fy_lo;
+  const int len = bot ? ny - m : m;
+  const long long j0 = bot ? ny - 1 : 0, dj = bot ? -nx : nx;
+  double prev = 0.0;
+  int jj = 0;
+  if (in) {
+    for (; jj + B <= len; jj += B) {
+      double v[B], mm[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        v[q] = b[j0 * nx + (jj + q) * dj];
+        if (k > 0) v[q] = fma(-czw, bp[j0 * nx + (jj + q) * dj], v[q]);
+        mm[q] = __ldg(invm + (long long)(jj + q) * nx);
+      }
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        prev = fma(-lo, prev, v[q]) * mm[q];
+        b[j0 * nx + (jj + q) * dj] = prev;
+      }
+    }
+    for (; jj < len; ++jj) {
+      double v = b[j0 * nx + jj * dj];
+      if (k > 0) v = fma(-czw, bp[j0 * nx + jj * dj], v);
+      prev = fma(-lo, prev, v) * invm[(long long)jj * nx];
+      b[j0 * nx + jj * dj] = prev;
+    }
+  }
+  const double c_own = in && len > 0 ? __ldg(cp + (long long)(len - 1) * nx) : 0.0;
+  const double y_oth = __shfl_xor_sync(0xffffffffu, prev, 1);
+  const double c_oth = __shfl_xor_sync(0xffffffffu, c_own, 1);
+  const double yT = bot ? y_oth : prev, yB = bot ? prev : y_oth;
+  const double cT = bot ? c_oth : c_own, cB = bot ? c_own : c_oth;
+  const double xT = (yT - cT * yB) / (1.0 - cT * cB);
+  double next = bot ? yB - cB * xT : xT;
+  if (!in || len == 0) return;
+  b[j0 * nx + (len - 1) * dj] = next;
+  jj = len - 2;
+  for (; jj - B + 1 >= 0; jj -= B) {
+    double v[B], c[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      v[q] = b[j0 * nx + (jj - q) * dj];
+      c[q] = __ldg(cp + (long long)(jj - q) * nx);
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      next = fma(-c[q], next, v[q]);
+      b[j0 * nx + (jj - q) * dj] = next;
+    }
+  }
+  for (; jj >= 0; --jj) {
+    next = fma(-cp[(long long)jj * nx], next, b[j0 * nx + jj * dj]);
+    b[j0 * nx + jj * dj] = next;
+  }
+}
+
+// GS epilogue: u += omega * x in place for every interior cell (the
+// refresh after a GS sweep fills all physical ghosts)
+__global__ void plane_relax_inplace_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                           const unsigned char* __restrict__ active, double omega,
+                                           const double* __restrict__ xbuf, long long total, long long first) {
+  for (long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; g0 < total;
+       g0 += (long long)gridDim.x * blockDim.x) {
+    const long long g = g0 + first;
+    int lo = 0, hi = npatch - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (patches[mid].cell0 <= g) lo = mid; else hi = mid - 1;
+    }
+    const PatchDev& P = patches[lo];
+    const long long e = g - P.cell0;
+    const int nx = P.nx, ny = P.ny;
+    const long long row = e / nx;
+    const int x = (int)(e - row * nx);
+    const int k = (int)(row / ny), j = (int)(row - (long long)k * ny);
+    const long long px = nx + 2, pxy = px * (ny + 2);
+    double* u = P.buf[active[lo]];
+    const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
+    u[iu] = relax(u[iu], omega, xbuf[g0]);
+  }
+}
+
 // Jacobi epilogue: v = u + omega * x for every interior cell, plus the
 // physical x-face ghosts of v (fused, see psm_line.cu).
 __global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
@@ -520,7 +626,68 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
 
 // Lexicographic plane GS: planes in k order, all patches of the level at
 // each stage (patches couple only through step-end ghosts).
+static int psm_plane_gs_staged(psm_plan* P, const unsigned char* da, double omega, cudaStream_t s);
+
+// Plane GS with the stage recurrence in the transformed domain (see
+// plane_gs_stage_kernel): residual of every plane from the pre-sweep iterate,
+// one DST of all planes, maxnz stages of modal solves, one DST back, relax.
 int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_t s) {
+  PlaneState* S = P->plane;
+  bool sym = !getenv("PSM_PLANE_GS_STAGED");
+  for (const PlaneRun& r : S->runs) sym = sym && r.h_fac->fy_lo == r.h_fac->fy_up;
+  if (!sym) return psm_plane_gs_staged(P, da, omega, s);
+  {
+    const int rc = psm_plane_residual(P, da, P->d_scratch, S->rbuf, s);
+    if (rc) return rc;
+  }
+  cublasSetStream(S->handle, s);
+  int maxnz = 0;
+  for (auto& h : P->hp) maxnz = std::max(maxnz, h.nz);
+  for (const PlaneRun& r : S->runs) {
+    const long long c0 = P->hp[r.p0].cell0;
+    long long planes = 0;
+    for (int p = r.p0; p < r.p1; ++p) planes += P->hp[p].nz;
+    const int rc = dst_gemm(S->handle, r.Q, r.nx, S->rbuf + c0, S->rhat + c0, planes * r.ny);
+    if (rc) return rc;
+    P->launches += 1;
+  }
+  const double czw = P->st.zm * omega;
+  for (int k = 0; k < maxnz; ++k) {
+    for (const PlaneRun& r : S->runs) {
+      int p0 = r.p0;
+      while (p0 < r.p1) {
+        if (k >= P->hp[p0].nz) { ++p0; continue; }
+        int p1 = p0 + 1;
+        while (p1 < r.p1 && k < P->hp[p1].nz) ++p1;
+        const long long nplanes = p1 - p0;
+        plane_gs_stage_kernel<<<(unsigned)((2 * nplanes * r.nx + 127) / 128), 128, 0, s>>>(
+            r.d_fac, P->d_patches, p0, nplanes, k, czw, S->rhat);
+        PCUDA(cudaGetLastError());
+        P->launches += 1;
+        p0 = p1;
+      }
+    }
+  }
+  for (const PlaneRun& r : S->runs) {
+    const long long c0 = P->hp[r.p0].cell0;
+    long long planes = 0, cells = 0;
+    for (int p = r.p0; p < r.p1; ++p) {
+      planes += P->hp[p].nz;
+      cells += (long long)P->hp[p].nx * P->hp[p].ny * P->hp[p].nz;
+    }
+    const int rc = dst_gemm(S->handle, r.Q, r.nx, S->rhat + c0, S->rbuf + c0, planes * r.ny);
+    if (rc) return rc;
+    plane_relax_inplace_kernel<<<blocks_for(cells, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega,
+                                                                      S->rbuf + c0, cells, c0);
+    PCUDA(cudaGetLastError());
+    P->launches += 2;
+  }
+  return PSM_OK;
+}
+
+// Stage-by-stage form (any y faces): per stage DST, modal solves, DST back,
+// relax in place fused with the next stage's residual.
+static int psm_plane_gs_staged(psm_plan* P, const unsigned char* da, double omega, cudaStream_t s) {
   PlaneState* S = P->plane;
   cublasSetStream(S->handle, s);
   int maxnz = 0;
