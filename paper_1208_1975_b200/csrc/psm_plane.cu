@@ -226,6 +226,11 @@ __global__ void plane_gs_stage_kernel(const PlaneFac* __restrict__ F, const Patc
   const double lo = F->fy_lo;
   const int len = bot ? ny - m : m;
   const long long j0 = bot ? ny - 1 : 0, dj = bot ? -nx : nx;
+  // warm L2 with this patch's next plane while the stage runs (the next
+  // stage's loads then come from L2, not HBM)
+  if (in && i == 0 && bot == 0 && k + 1 < patches[p0 + pl].nz && ((plane_cells * 8) & 15) == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b + plane_cells), "r"((unsigned)(plane_cells * 8))
+                 : "memory");
   double prev = 0.0;
   int jj = 0;
   if (in) {
