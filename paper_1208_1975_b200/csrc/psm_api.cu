@@ -523,6 +523,11 @@ int psm_plan_destroy(psm_plan* P) {
   for (auto& kv : P->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
+  for (int i = 0; i < 4; ++i) {
+    if (P->side[i]) cudaStreamDestroy(P->side[i]);
+    if (P->side_join[i]) cudaEventDestroy(P->side_join[i]);
+  }
+  if (P->side_fork) cudaEventDestroy(P->side_fork);
   delete P;
   return PSM_OK;
 }

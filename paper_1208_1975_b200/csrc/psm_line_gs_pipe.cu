@@ -742,9 +742,29 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
                       cudaStream_t s) {
   const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
                     P->st.zm == -1.0 && P->st.zp == -1.0;
+  // groups of different nx touch different patches: run them concurrently
+  // (a group's persistent grid often leaves SMs free for the next)
+  const int ng = (int)P->gspipe->groups.size();
+  const bool fan = ng > 1;
+  if (fan) {
+    if (!P->side_fork) {
+      if (cudaEventCreateWithFlags(&P->side_fork, cudaEventDisableTiming) != cudaSuccess)
+        return psm_set_error(PSM_ECUDA, "event create");
+      for (int i = 0; i < 4; ++i)
+        if (cudaStreamCreateWithFlags(&P->side[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->side_join[i], cudaEventDisableTiming) != cudaSuccess)
+          return psm_set_error(PSM_ECUDA, "side stream create");
+    }
+    if (cudaEventRecord(P->side_fork, s) != cudaSuccess) return psm_set_error(PSM_ECUDA, "fork record");
+    for (int i = 0; i < std::min(ng, 4); ++i)
+      if (cudaStreamWaitEvent(P->side[i], P->side_fork, 0) != cudaSuccess) return psm_set_error(PSM_ECUDA, "fork wait");
+  }
+  int gi = 0;
   for (const GsPipeGroup& G : P->gspipe->groups) {
     cudaError_t e;
     int* tk = tickets + G.ticket;
+    cudaStream_t s_main = s;
+    if (fan) s = P->side[gi++ % 4];
 #define PSM_GSL(N) \
   gs_pipe_launch<N>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, \
                     G.T, G.nl, s)
@@ -761,6 +781,14 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
 #undef PSM_GSL
     if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
     P->launches += 1;
+    s = s_main;
+  }
+  if (fan) {
+    for (int i = 0; i < std::min(ng, 4); ++i) {
+      if (cudaEventRecord(P->side_join[i], P->side[i]) != cudaSuccess ||
+          cudaStreamWaitEvent(s, P->side_join[i], 0) != cudaSuccess)
+        return psm_set_error(PSM_ECUDA, "join");
+    }
   }
   return PSM_OK;
 }
