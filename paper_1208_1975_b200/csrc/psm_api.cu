@@ -298,12 +298,6 @@ int psm_factors_apply(const psm_factors* F, const double* r, double* x, long lon
 // ---------------------------------------------------------------------------
 // plans
 // ---------------------------------------------------------------------------
-static int largest_divisor_le(int n, int cap) {
-  for (int d = std::min(n, std::max(1, cap)); d >= 1; --d)
-    if (n % d == 0) return d;
-  return 1;
-}
-
 
 int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_desc* copies, int ncopy,
                     const psm_stencil* st, int kind, psm_factors* const* fac, psm_plan** out) {
@@ -523,7 +517,7 @@ int psm_plan_destroy(psm_plan* P) {
   for (auto& kv : P->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (P->cap_stream) cudaStreamDestroy(P->cap_stream);
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < psm_plan::kSide; ++i) {
     if (P->side[i]) cudaStreamDestroy(P->side[i]);
     if (P->side_join[i]) cudaEventDestroy(P->side_join[i]);
   }
@@ -904,6 +898,33 @@ int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int sid
   CUDA_TRY(launch_halo_unpack(dst, plane_dev, (int)px, (int)py, (cudaStream_t)stream));
   P->launches += 1;
   return PSM_OK;
+}
+
+// Side streams of a plan: psm_side_fork makes n (<= kSide) side streams wait
+// for everything queued on s so far; psm_side_join makes s wait for them.
+// Both are legal inside a stream capture (parallel graph branches).
+cudaError_t psm_side_fork(psm_plan* P, cudaStream_t s, int n) {
+  if (!P->side_fork) {
+    cudaError_t e = cudaEventCreateWithFlags(&P->side_fork, cudaEventDisableTiming);
+    for (int i = 0; i < psm_plan::kSide && e == cudaSuccess; ++i) {
+      e = cudaStreamCreateWithFlags(&P->side[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->side_join[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaEventRecord(P->side_fork, s);
+  for (int i = 0; i < std::min(n, (int)psm_plan::kSide) && e == cudaSuccess; ++i)
+    e = cudaStreamWaitEvent(P->side[i], P->side_fork, 0);
+  return e;
+}
+
+cudaError_t psm_side_join(psm_plan* P, cudaStream_t s, int n) {
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < std::min(n, (int)psm_plan::kSide) && e == cudaSuccess; ++i) {
+    e = cudaEventRecord(P->side_join[i], P->side[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, P->side_join[i], 0);
+  }
+  return e;
 }
 
 // ---------------------------------------------------------------------------

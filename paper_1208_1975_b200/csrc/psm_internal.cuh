@@ -240,8 +240,9 @@ struct psm_plan {
   int phys_pending = 2;
   // side streams for independent launches of one sweep (line-GS groups of
   // different nx): fork / join by events, captured as parallel graph branches
-  cudaStream_t side[4] = {};
-  cudaEvent_t side_fork = nullptr, side_join[4] = {};
+  static constexpr int kSide = 4;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t side_fork = nullptr, side_join[kSide] = {};
   // box path: blocks (patch, x0, y0, z0) sorted by wavefront bi+bj+bk (GS),
   // and Jacobi regions of (8/bx) x (8/by) x (8/bz) blocks
   int4* d_boxes = nullptr;

@@ -514,6 +514,8 @@ static cudaError_t gs_pipe_launch(int chaotic, int unit, int grid, const PatchDe
 using namespace psm;
 
 int psm_set_error(int code, const char* msg);
+extern "C" cudaError_t psm_side_fork(psm_plan* P, cudaStream_t s, int n);  // psm_api.cu
+extern "C" cudaError_t psm_side_join(psm_plan* P, cudaStream_t s, int n);
 
 // One group of patches sharing nx (= NC * nl): units, tables, launch geometry.
 struct GsPipeGroup {
@@ -747,24 +749,15 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
   const int ng = (int)P->gspipe->groups.size();
   const bool fan = ng > 1;
   if (fan) {
-    if (!P->side_fork) {
-      if (cudaEventCreateWithFlags(&P->side_fork, cudaEventDisableTiming) != cudaSuccess)
-        return psm_set_error(PSM_ECUDA, "event create");
-      for (int i = 0; i < 4; ++i)
-        if (cudaStreamCreateWithFlags(&P->side[i], cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&P->side_join[i], cudaEventDisableTiming) != cudaSuccess)
-          return psm_set_error(PSM_ECUDA, "side stream create");
-    }
-    if (cudaEventRecord(P->side_fork, s) != cudaSuccess) return psm_set_error(PSM_ECUDA, "fork record");
-    for (int i = 0; i < std::min(ng, 4); ++i)
-      if (cudaStreamWaitEvent(P->side[i], P->side_fork, 0) != cudaSuccess) return psm_set_error(PSM_ECUDA, "fork wait");
+    const cudaError_t e = psm_side_fork(P, s, ng);
+    if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
   }
   int gi = 0;
   for (const GsPipeGroup& G : P->gspipe->groups) {
     cudaError_t e;
     int* tk = tickets + G.ticket;
     cudaStream_t s_main = s;
-    if (fan) s = P->side[gi++ % 4];
+    if (fan) s = P->side[gi++ % psm_plan::kSide];
 #define PSM_GSL(N) \
   gs_pipe_launch<N>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, \
                     G.T, G.nl, s)
@@ -784,11 +777,8 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
     s = s_main;
   }
   if (fan) {
-    for (int i = 0; i < std::min(ng, 4); ++i) {
-      if (cudaEventRecord(P->side_join[i], P->side[i]) != cudaSuccess ||
-          cudaStreamWaitEvent(s, P->side_join[i], 0) != cudaSuccess)
-        return psm_set_error(PSM_ECUDA, "join");
-    }
+    const cudaError_t e = psm_side_join(P, s, ng);
+    if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
   }
   return PSM_OK;
 }

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(ZCfg<NX>::THREADS, 1)
                               const ZUnit* __restrict__ units, int nunits, const __grid_constant__ ZTab T,
                               double* __restrict__ rglob) {
   using C = ZCfg<NX>;
-  constexpr int R = C::R, PX = C::PX, NSEG = C::NSEG, NSL = C::NSL, RS = C::RS, E = C::E, ACT = C::ACT;
+  constexpr int R = C::R, PX = C::PX, NSEG = C::NSEG, RS = C::RS;
   extern __shared__ __align__(128) double zsm[];
   double* uring = zsm;
   double* fring = uring + C::NU * C::US;

@@ -71,7 +71,6 @@ __device__ __forceinline__ void g_named_arrive(int id, int count) {
 constexpr int kGAcWarps = 16, kGSolWarps = 3, kGThreads = (kGAcWarps + kGSolWarps + 1) * 32;
 constexpr int kGAct = kGAcWarps * 32;          // A/C threads
 constexpr int kGE = kMaxTileCells / kGAct;     // cells per A/C thread (4)
-constexpr int kGLanes = kGSolWarps * 32;       // solver lanes
 constexpr int kGNbar = (kGAcWarps + kGSolWarps) * 32;
 constexpr int kGNU = 4, kGNF = 2;
 constexpr int kGBarR = 1, kGBarY = 3;

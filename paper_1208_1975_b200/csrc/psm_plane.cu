@@ -410,11 +410,6 @@ struct PlaneState {
 
   std::vector<long long> stage_off;
   std::vector<PlaneRun> runs;
-  // runs of the banded solve are independent: side streams let several run
-  // at once (fork / join by events; captured as parallel graph branches)
-  static constexpr int kSide = 4;
-  cudaStream_t side[kSide] = {};
-  cudaEvent_t fork = nullptr, join[kSide] = {};
 };
 
 
@@ -422,6 +417,8 @@ struct PlaneState {
 int psm_set_error(int code, const char* msg);
 extern "C" int psm_plane_residual(psm_plan* P, const unsigned char* da, double* partials, double* rbuf,
                                   cudaStream_t s);  // psm_api.cu
+extern "C" cudaError_t psm_side_fork(psm_plan* P, cudaStream_t s, int n);  // psm_api.cu
+extern "C" cudaError_t psm_side_join(psm_plan* P, cudaStream_t s, int n);
 
 #define PCUDA(expr)                                                                      \
   do {                                                                                   \
@@ -590,11 +587,7 @@ int psm_plane_plan_free(psm_plan* P) {
   cudaFree(S->shat);
   cudaFree(S->d_stage_off);
   for (auto& r : S->runs) cudaFree(r.d_units);
-  for (int i = 0; i < PlaneState::kSide; ++i) {
-    if (S->side[i]) cudaStreamDestroy(S->side[i]);
-    if (S->join[i]) cudaEventDestroy(S->join[i]);
-  }
-  if (S->fork) cudaEventDestroy(S->fork);
+
   delete S;
   P->plane = nullptr;
   return PSM_OK;
@@ -615,17 +608,7 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
   int nband = 0;
   for (const PlaneRun& r : S->runs) nband += (r.bw > 0 && psm_plane_band_mode != 0);
   const bool fan = nband > 1;
-  if (fan) {
-    if (!S->fork) {
-      PCUDA(cudaEventCreateWithFlags(&S->fork, cudaEventDisableTiming));
-      for (int i = 0; i < PlaneState::kSide; ++i) {
-        PCUDA(cudaStreamCreateWithFlags(&S->side[i], cudaStreamNonBlocking));
-        PCUDA(cudaEventCreateWithFlags(&S->join[i], cudaEventDisableTiming));
-      }
-    }
-    PCUDA(cudaEventRecord(S->fork, s));
-    for (int i = 0; i < std::min(nband, (int)PlaneState::kSide); ++i) PCUDA(cudaStreamWaitEvent(S->side[i], S->fork, 0));
-  }
+  if (fan) PCUDA(psm_side_fork(P, s, nband));  // runs are independent: several at once
   int bi = 0;
   for (const PlaneRun& r : S->runs) {
     const long long c0 = P->hp[r.p0].cell0;
@@ -635,7 +618,7 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
       cells += (long long)P->hp[p].nx * P->hp[p].ny * P->hp[p].nz;
     }
     if (r.bw > 0 && psm_plane_band_mode != 0) {
-      cudaStream_t rs = fan ? S->side[bi++ % PlaneState::kSide] : s;
+      cudaStream_t rs = fan ? P->side[bi++ % psm_plan::kSide] : s;
       PCUDA(launch_plane_band_jacobi(band_k_for(r.nx), r.bw, P->d_patches, da, omega, S->rbuf, S->rhat, r.d_units,
                                      r.nunits, r.hinf.data(), rs));
       P->launches += 1;
@@ -653,12 +636,7 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
     PCUDA(cudaGetLastError());
     P->launches += 4;
   }
-  if (fan) {
-    for (int i = 0; i < std::min(nband, (int)PlaneState::kSide); ++i) {
-      PCUDA(cudaEventRecord(S->join[i], S->side[i]));
-      PCUDA(cudaStreamWaitEvent(s, S->join[i], 0));
-    }
-  }
+  if (fan) PCUDA(psm_side_join(P, s, nband));
   return PSM_OK;
 }
 
