@@ -148,7 +148,14 @@ int psm_halo_unpack(psm_plan* plan, const unsigned char* active, int patch, int 
  * psm_ipc_open_handle: map a peer's handle (cached per handle) -> base+offset.
  * psm_plan_set_peer_halo: side 0 = the neighbour below (its nz given), 1 =
  *   above; peer_buf0/1 = its two padded buffers (NULL, NULL clears).  Needs a
- *   line plan on a z-marching nx (PSM_EUNSUPPORTED otherwise). */
+ *   line plan on a z-marching nx (PSM_EUNSUPPORTED otherwise).
+ * psm_device_pci_bus_id: the current device's PCI bus id ("0000:1b:00.0").
+ * psm_peer_access: *ok_out = 1 when the current device can load/store the
+ *   memory of the device with that bus id (the same device, or
+ *   cudaDeviceCanAccessPeer), 0 otherwise (also when it is not visible to
+ *   this process); callers gate the IPC halo on it. */
+int psm_device_pci_bus_id(char* out, int len);
+int psm_peer_access(const char* pci_bus_id, int* ok_out);
 int psm_ipc_get_handle(const void* ptr, void* handle_out, long long* offset_out);
 int psm_ipc_open_handle(const void* handle, long long offset, void** ptr_out);
 int psm_ipc_close_all(void);

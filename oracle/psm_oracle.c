@@ -15,7 +15,9 @@
  *                          ordered sum, not fsum)
  * with the exact line-block inverse applied by a Thomas solve along x
  * (the closure-free block of stencil.py:115-138 is tridiag(f-x, c, f+x)).
- * Lines are distributed over OpenMP threads.
+ * Lines are distributed over OpenMP threads.  Also: serial line GS
+ * (oracle_line_gs) and the residual sum of squares, for the full-size
+ * parity checks of tests/test_configs_gpu.py.
  */
 #include <math.h>
 #include <stdlib.h>
@@ -98,6 +100,65 @@ double oracle_line_jacobi(const double* u, const double* f, double* v, int nx, i
   }
   free(cp);
   free(im);
+  return total;
+}
+
+/* One serial (lexicographic) line Gauss-Seidel sweep of a single patch, in
+ * place: smoother.py:156-169 under the serial strategy (runtime.py:164-168),
+ * lines (j,k) in x-fastest block order (grid.py:300-307), each line's
+ * residual read from the current u (block_residual, stencil.py:93-112) and
+ * u_line <- u_line + omega * Ainv r (block_update, smoother.py:90-93).  The
+ * ghosts are read as stored (lagged to step end, as in the reference).  The
+ * line inverse is the same Thomas solve as oracle_line_jacobi.  One thread
+ * per patch: callers run different patches on different threads. */
+void oracle_line_gs(double* u, const double* f, int nx, int ny, int nz, double cc, const double* fc,
+                    double omega) {
+  const size_t px = nx + 2, py = ny + 2, pxy = px * py;
+  double* cp = (double*)malloc(sizeof(double) * nx);
+  double* im = (double*)malloc(sizeof(double) * nx);
+  double* y = (double*)malloc(sizeof(double) * nx);
+  double prev = 0.0;
+  for (int i = 0; i < nx; ++i) {
+    double m = cc - fc[0] * prev;
+    im[i] = 1.0 / m;
+    cp[i] = fc[1] / m;
+    prev = cp[i];
+  }
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j) {
+      const size_t base = IDX(1, j + 1, k + 1);
+      const double* fr = f + ((size_t)k * ny + j) * nx;
+      double pr = 0.0;
+      for (int i = 0; i < nx; ++i) {
+        const double r = resid(u, base + i, px, pxy, fr[i], cc, fc);
+        pr = (r - fc[0] * pr) * im[i];
+        y[i] = pr;
+      }
+      for (int i = nx - 2; i >= 0; --i) y[i] -= cp[i] * y[i + 1];
+      for (int i = 0; i < nx; ++i) u[base + i] = u[base + i] + omega * y[i];
+    }
+  free(cp);
+  free(im);
+  free(y);
+}
+
+/* Sum of r^2 over one patch interior (residual_norm, smoother.py:96-109, as a
+ * plain ordered sum per line, lines summed in order). */
+double oracle_residual_sumsq(const double* u, const double* f, int nx, int ny, int nz, double cc,
+                             const double* fc) {
+  const size_t px = nx + 2, py = ny + 2, pxy = px * py;
+  double total = 0.0;
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j) {
+      const size_t base = IDX(1, j + 1, k + 1);
+      const double* fr = f + ((size_t)k * ny + j) * nx;
+      double ss = 0.0;
+      for (int i = 0; i < nx; ++i) {
+        const double r = resid(u, base + i, px, pxy, fr[i], cc, fc);
+        ss += r * r;
+      }
+      total += ss;
+    }
   return total;
 }
 

@@ -54,6 +54,8 @@ EXPORTS = (
     "psm_plan_launches",
     "psm_plane_solver",
     "psm_smooth_steps",
+    "psm_device_pci_bus_id",
+    "psm_peer_access",
     "psm_ipc_get_handle",
     "psm_ipc_open_handle",
     "psm_ipc_close_all",
@@ -139,6 +141,8 @@ def load():
             "psm_plan_launches": (ll, [vp]),
             "psm_plane_solver": (i, [i]),
             "psm_smooth_steps": (i, [vp, ub, i, d, i, i, i, vp]),
+            "psm_device_pci_bus_id": (i, [ctypes.c_char_p, i]),
+            "psm_peer_access": (i, [ctypes.c_char_p, ctypes.POINTER(i)]),
             "psm_ipc_get_handle": (i, [vp, vp, ctypes.POINTER(ll)]),
             "psm_ipc_open_handle": (i, [vp, ll, ctypes.POINTER(vp)]),
             "psm_ipc_close_all": (i, []),

@@ -37,7 +37,7 @@ cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
                            cudaStream_t stream);
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
-                                   long long max_face, int skip_x, cudaStream_t stream);
+                                   long long max_face, int skip_x, int use_covered, cudaStream_t stream);
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
                                     int ncopy, long long total, cudaStream_t stream);
 cudaError_t launch_plane_sums(const PatchDev* patches, int npatch, const double* partials, double* plane_sums,
@@ -597,7 +597,8 @@ int psm_refresh_ghosts(psm_plan* P, const unsigned char* active, int what, void*
   const int level = (what & PSM_GHOST_SKIP_X) ? P->phys_pending : 2;
   if (what & PSM_GHOST_PHYSICAL) {
     if (level > 0) {
-      CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->ghost_max_face, level == 1 ? 1 : 0, s));
+      CUDA_TRY(launch_physical_ghosts(P->d_patches, P->npatch, da, P->ghost_max_face, level == 1 ? 1 : 0,
+                                      (what & PSM_GHOST_INTERFACE) ? 1 : 0, s));
       P->launches += P->ghost_total > 0;
     }
     P->phys_pending = 0;
@@ -905,12 +906,29 @@ int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int sid
 // Both are legal inside a stream capture (parallel graph branches).
 cudaError_t psm_side_fork(psm_plan* P, cudaStream_t s, int n) {
   if (!P->side_fork) {
-    cudaError_t e = cudaEventCreateWithFlags(&P->side_fork, cudaEventDisableTiming);
+    // create every stream and event first and publish side_fork last, so a
+    // failure part way leaves nothing half-initialised for the next call
+    cudaStream_t st[psm_plan::kSide] = {};
+    cudaEvent_t ev[psm_plan::kSide] = {};
+    cudaEvent_t fork = nullptr;
+    cudaError_t e = cudaSuccess;
     for (int i = 0; i < psm_plan::kSide && e == cudaSuccess; ++i) {
-      e = cudaStreamCreateWithFlags(&P->side[i], cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->side_join[i], cudaEventDisableTiming);
+      e = cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
     }
-    if (e != cudaSuccess) return e;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      for (int i = 0; i < psm_plan::kSide; ++i) {
+        if (st[i]) cudaStreamDestroy(st[i]);
+        if (ev[i]) cudaEventDestroy(ev[i]);
+      }
+      return e;
+    }
+    for (int i = 0; i < psm_plan::kSide; ++i) {
+      P->side[i] = st[i];
+      P->side_join[i] = ev[i];
+    }
+    P->side_fork = fork;
   }
   cudaError_t e = cudaEventRecord(P->side_fork, s);
   for (int i = 0; i < std::min(n, (int)psm_plan::kSide) && e == cudaSuccess; ++i)
@@ -975,6 +993,33 @@ int psm_ipc_open_handle(const void* handle, long long offset, void** ptr_out) {
     m[key] = base;
   }
   *ptr_out = (char*)base + offset;
+  return PSM_OK;
+}
+
+int psm_device_pci_bus_id(char* out, int len) {
+  if (!out || len < 16) return fail(PSM_EINVAL, "bad arguments");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetPCIBusId(out, len, dev));
+  return PSM_OK;
+}
+
+int psm_peer_access(const char* pci_bus_id, int* ok_out) {
+  if (!pci_bus_id || !ok_out) return fail(PSM_EINVAL, "bad arguments");
+  *ok_out = 0;
+  int me = 0, peer = -1;
+  CUDA_TRY(cudaGetDevice(&me));
+  if (cudaDeviceGetByPCIBusId(&peer, pci_bus_id) != cudaSuccess) {
+    cudaGetLastError();  // not visible here: no peer mapping possible
+    return PSM_OK;
+  }
+  if (peer == me) {
+    *ok_out = 1;
+    return PSM_OK;
+  }
+  int can = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can, me, peer));
+  *ok_out = can ? 1 : 0;
   return PSM_OK;
 }
 
@@ -1070,7 +1115,11 @@ int psm_smooth_steps(psm_plan* P, unsigned char* active, int scheme, double omeg
   for (unsigned char a : act)
     if (a > 1) return fail(PSM_EINVAL, "active flags must be 0 or 1");
   char kb[96];
-  snprintf(kb, sizeof kb, "%d:%a:%d:%d:%d:", scheme, omega, steps, gs_mode, history);
+  // the key holds everything that changes the captured launch sequence:
+  // the process-wide plane solver mode (psm_plane_solver) and the staged
+  // plane-GS choice included, so changing either re-captures
+  snprintf(kb, sizeof kb, "%d:%a:%d:%d:%d:%d:%d:", scheme, omega, steps, gs_mode, history, psm_plane_band_mode,
+           getenv("PSM_PLANE_GS_STAGED") ? 1 : 0);
   auto& G = P->graphs[std::string(kb) + std::string((const char*)active, P->npatch)];
   if (G.exec == nullptr && G.seen == 0) {
     // first call with this key: eager, which also performs every lazy

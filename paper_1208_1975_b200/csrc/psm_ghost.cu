@@ -21,7 +21,7 @@ namespace psm {
 // perimeter (edges shared with y/z faces) is rewritten here.
 __global__ void __launch_bounds__(256) physical_ghost_kernel(const PatchDev* __restrict__ patches,
                                                              const unsigned char* __restrict__ active, int skip_x,
-                                                             int pbase) {
+                                                             int use_covered, int pbase) {
   const int face = blockIdx.z, axis = face >> 1, side = face & 1;
   const int pi = pbase + blockIdx.y;
   const PatchDev& P = patches[pi];
@@ -31,7 +31,10 @@ __global__ void __launch_bounds__(256) physical_ghost_kernel(const PatchDev* __r
   const int A = axis == 0 ? py : px, B = axis == 2 ? py : pz;
   // faces whose interior something else writes (the Jacobi sweep's x faces,
   // a face one interface copy covers, a peer-halo z face): perimeter only
-  const bool perim = (axis == 0 && skip_x) || ((P.covered >> face) & 1) || (axis == 2 && ((P.iface >> side) & 1));
+  // (covered faces only when this refresh also runs the interface copies:
+  // a physical-only refresh must fill every face, grid.py:311-330)
+  const bool perim = (axis == 0 && skip_x) || (use_covered && ((P.covered >> face) & 1)) ||
+                     (axis == 2 && ((P.iface >> side) & 1));
   const int n = perim ? 2 * A + 2 * (B - 2) : A * B;
   for (int c = blockIdx.x * 1024 + threadIdx.x; c < min(n, (int)(blockIdx.x + 1) * 1024); c += 256) {
     int a, b;
@@ -177,11 +180,11 @@ cudaError_t launch_halo_unpack(double* dst_plane, const double* src_plane, int p
 
 // max_face: largest face (cells) of any patch; 1024 cells per CTA
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
-                                   long long max_face, int skip_x, cudaStream_t stream) {
+                                   long long max_face, int skip_x, int use_covered, cudaStream_t stream) {
   if (npatch == 0 || max_face == 0) return cudaSuccess;
   for (int base = 0; base < npatch; base += 65535) {
     const dim3 grid((unsigned)((max_face + 1023) / 1024), (unsigned)std::min(65535, npatch - base), 6);
-    physical_ghost_kernel<<<grid, 256, 0, stream>>>(patches, active, skip_x, base);
+    physical_ghost_kernel<<<grid, 256, 0, stream>>>(patches, active, skip_x, use_covered, base);
   }
   return cudaGetLastError();
 }

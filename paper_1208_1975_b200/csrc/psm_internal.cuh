@@ -3,9 +3,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/psmooth.h"
 
 namespace psm {
+
+// True the first time it is called for the current device with this mask
+// (one bit per device ordinal): per-device one-time setup such as the
+// dynamic-shared-memory opt-in, which is a per-device function attribute.
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const unsigned long long bit = 1ull << dev;
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 constexpr int kSeg = 32;  // line segment owned by one solver lane
 

@@ -517,8 +517,8 @@ static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned cha
                            double omega, double* partials, const ZUnit* units, int nunits, int grid,
                            const ZTab& T, double* rglob, int peer, cudaStream_t stream) {
   using C = ZCfg<NX>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM_BYTES);
     cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -531,7 +531,6 @@ static cudaError_t zlaunch(int unit, const PatchDev* patches, const unsigned cha
                          (int)C::SMEM_BYTES);
     cudaFuncSetAttribute(line_jacobi_zmarch_kernel<NX, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM_BYTES);
-    attr = true;
   }
 #define PSM_ZL(U_, R_)                                                                                         \
   line_jacobi_zmarch_kernel<NX, U_, R_><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(patches, active, st, omega, \

@@ -458,19 +458,14 @@ cudaError_t launch_line_zgen(const int* nxs, int nnx, int unit, const PatchDev* 
   const size_t dbl = (size_t)kGNU * su + (size_t)kGNF * sf + 2 * (size_t)sb + 2 * kGAcWarps;
   const size_t smem = dbl * 8 + (2 * kGNU + 2 * kGNF) * 8 + 16;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static size_t attr0 = 0, attr1 = 0;
+  // the opt-in is a per-device attribute and smem depends on the plan: set
+  // it on every launch (a host-side call, no stream work, legal in capture)
   if (unit) {
-    if (smem > attr1) {
-      cudaFuncSetAttribute(line_jacobi_zgen_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr1 = smem;
-    }
+    cudaFuncSetAttribute(line_jacobi_zgen_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     line_jacobi_zgen_kernel<1><<<grid, kGThreads, smem, stream>>>(patches, active, st, omega, partials,
                                                                   (const GUnit*)units, nunits, T, su, sf, sb);
   } else {
-    if (smem > attr0) {
-      cudaFuncSetAttribute(line_jacobi_zgen_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr0 = smem;
-    }
+    cudaFuncSetAttribute(line_jacobi_zgen_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     line_jacobi_zgen_kernel<0><<<grid, kGThreads, smem, stream>>>(patches, active, st, omega, partials,
                                                                   (const GUnit*)units, nunits, T, su, sf, sb);
   }

@@ -228,7 +228,10 @@ __global__ void plane_gs_stage_kernel(const PlaneFac* __restrict__ F, const Patc
   const long long j0 = bot ? ny - 1 : 0, dj = bot ? -nx : nx;
   // warm L2 with this patch's next plane while the stage runs (the next
   // stage's loads then come from L2, not HBM)
-  if (in && i == 0 && bot == 0 && k + 1 < patches[p0 + pl].nz && ((plane_cells * 8) & 15) == 0)
+  // (bulk prefetches need a 16-byte aligned address and size; cell0 offsets
+  // of earlier odd-sized patches can leave the plane only 8-byte aligned)
+  if (in && i == 0 && bot == 0 && k + 1 < patches[p0 + pl].nz && ((plane_cells * 8) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(b + plane_cells) & 15) == 0)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b + plane_cells), "r"((unsigned)(plane_cells * 8))
                  : "memory");
   double prev = 0.0;

@@ -252,10 +252,9 @@ static cudaError_t band_launch_t(const PatchDev* patches, const unsigned char* a
                                  const double* rbuf, double* zbuf, const int2* units, int nunits, int sms,
                                  const BandHinf& Hinf, cudaStream_t s) {
   using C = BandCfg<K, BW>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(plane_band_jacobi_kernel<K, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr = true;
   }
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plane_band_jacobi_kernel<K, BW>, kBandT, C::SMEM);

@@ -203,7 +203,7 @@ class _PeerHalo:
         torch.cuda.synchronize(p.device)
         try:
             mine = {"bufs": [_ipc_export(b) for b in p._bufs], "flags": _ipc_export(self.flags),
-                    "nz": domain.nz_local}
+                    "nz": domain.nz_local, "pci": _pci_bus_id()}
         except (_lib.LibraryError, ValueError) as e:  # still join the gather, so no rank hangs in it
             mine = {"error": str(e)}
         allinfo = [None] * domain.world
@@ -218,6 +218,7 @@ class _PeerHalo:
                 if r is None:
                     continue
                 info = allinfo[r]
+                _require_peer_access(info["pci"], r)
                 bufs = [_ipc_import(h, off) for h, off in info["bufs"]]
                 flags = _ipc_import(*info["flags"])
                 # below: we are its upper neighbour (its flags[1]); above: its flags[0]
@@ -251,6 +252,21 @@ class _PeerHalo:
         a, b = self.peer_flags
         _lib.check(_lib.load().psm_halo_signal(ctypes.c_void_p(a), ctypes.c_void_p(b), int(value), stream),
                    "halo_signal")
+
+
+def _pci_bus_id():
+    buf = ctypes.create_string_buffer(32)
+    _lib.check(_lib.load().psm_device_pci_bus_id(buf, 32), "device_pci_bus_id")
+    return buf.value.decode()
+
+
+def _require_peer_access(pci, rank):
+    """Raise LibraryError unless this process's device can map rank's
+    device memory (same device, or cudaDeviceCanAccessPeer)."""
+    ok = ctypes.c_int()
+    _lib.check(_lib.load().psm_peer_access(pci.encode(), ctypes.byref(ok)), "peer_access")
+    if not ok.value:
+        raise _lib.LibraryError(f"no peer access from this device to rank {rank}'s device {pci}")
 
 
 def _ipc_export(t):
@@ -552,7 +568,7 @@ class _PeerLevelHalo:
         try:
             mine = {"patches": {g: [_ipc_export(b) for b in domain.patches[i]._bufs]
                                 for i, g in enumerate(domain.mine)},
-                    "ready": _ipc_export(self.ready), "read": _ipc_export(self.read)}
+                    "ready": _ipc_export(self.ready), "read": _ipc_export(self.read), "pci": _pci_bus_id()}
         except (_lib.LibraryError, ValueError) as e:
             mine = {"error": str(e)}
         allinfo = [None] * world
@@ -567,6 +583,9 @@ class _PeerLevelHalo:
             ridx = {g: len(domain.mine) + i for i, g in enumerate(remote)}
             descs = [p._desc() for p in domain.patches]
             self._remote_ptrs = []
+            for r in sorted({domain.owner[g] for g in remote} | set(self.consumers) | set(self.producers)):
+                if r != rank:
+                    _require_peer_access(allinfo[r]["pci"], r)
             for g in remote:
                 b0, b1 = (_ipc_import(h, off) for h, off in allinfo[domain.owner[g]]["patches"][g])
                 d = _lib.PatchDesc()
