@@ -201,6 +201,28 @@ int psm_history_planes(psm_plan* plan, int slot, double* out_dev, void* stream);
 /* Fixed-order (pairwise tree) sum of n doubles on the device -> out_dev[0]. */
 int psm_tree_sum(const double* in_dev, long long n, double* out_dev, void* stream);
 
+/* ---- per-block primitives of the reference API (psm_util.cu).  The
+ * sweeps above never call these; they back the reference's public building
+ * blocks.  All stream-ordered except psm_invert_dense, which synchronises
+ * once to report singularity.
+ *
+ * psm_box_residual: replaces block_residual (stencil.py:93-112) and, with
+ *   f == NULL, apply_stencil (stencil.py:71-84): out[x + ex*(y + ey*z)] =
+ *   f - A u (or A u) on the interior box [lo, lo+ext) of one padded buffer u
+ *   (ghosts read as stored), with the reference's rounding sequence.
+ * psm_matvec: replaces matvec (blocklinalg.py:90-105), M column-major n x n,
+ *   ascending-column accumulation, bit-identical; with u != NULL it is
+ *   block_update (smoother.py:90-93): y = u + omega * (M x).
+ * psm_invert_dense: replaces invert_dense (blocklinalg.py:50-87).  w is the
+ *   n x 2n column-major matrix [A | I] (overwritten; columns n..2n-1 end as
+ *   A^-1), work holds 3n + 4 doubles.  Partial pivoting with the reference's
+ *   singularity rule (|pivot| < 1e-14 ||A||_inf -> PSM_ESINGULAR,
+ *   *singular_step = 1 + step, -1 for the zero matrix). */
+int psm_box_residual(const double* u, const double* f, int nx, int ny, int nz, const int* lo, const int* ext,
+                     const psm_stencil* st, double* out, void* stream);
+int psm_matvec(const double* m, const double* x, const double* u, double omega, double* y, int n, void* stream);
+int psm_invert_dense(double* w, int n, double* work, int* singular_step, double* tiny_pivot, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,9 @@ EXPORTS = (
     "psm_plan_set_peer_halo",
     "psm_halo_signal",
     "psm_halo_wait",
+    "psm_box_residual",
+    "psm_matvec",
+    "psm_invert_dense",
 )
 PLANE_AUTO = 0
 PLANE_DST = 1
@@ -149,6 +152,10 @@ def load():
             "psm_plan_set_peer_halo": (i, [vp, i, i, vp, vp, i]),
             "psm_halo_signal": (i, [vp, vp, i, vp]),
             "psm_halo_wait": (i, [vp, i, i, vp]),
+            "psm_box_residual": (i, [vp, vp, i, i, i, ctypes.POINTER(i), ctypes.POINTER(i), ctypes.POINTER(Stencil),
+                                     vp, vp]),
+            "psm_matvec": (i, [vp, vp, vp, d, vp, i, vp]),
+            "psm_invert_dense": (i, [vp, i, vp, ctypes.POINTER(i), ctypes.POINTER(d), vp]),
         }
         for name, (res, args) in sig.items():
             if "PSM_LIB" in os.environ and not hasattr(lib, name):

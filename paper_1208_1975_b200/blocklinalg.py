@@ -25,7 +25,7 @@ from .grid import _int3, default_device
 from .stencil import Stencil7
 
 __all__ = ["SingularMatrixError", "BlockFactors", "InverseCache", "block_kind", "plane_solver",
-           "multiply_back_error"]
+           "multiply_back_error", "invert_dense", "matvec"]
 
 _MAX_DENSE = 8192
 
@@ -53,6 +53,91 @@ def multiply_back_error(a, ainv):
 
 class SingularMatrixError(ValueError):
     """Raised when a block operator has no stable exact inverse (blocklinalg.py:35-36)."""
+
+
+def _device_tensor(a, name, device=None):
+    """float64 CUDA tensor view/copy of ``a`` (array or tensor)."""
+    t = torch.as_tensor(a, dtype=torch.float64)
+    if device is None:
+        device = t.device if t.is_cuda else default_device()
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise RuntimeError(f"{name}: computed on the CUDA device (there is no CPU fallback)")
+    return t.to(device)
+
+
+def _like_input(t, template):
+    """Return ``t`` as the caller's kind: a tensor for tensor input, a numpy
+    array for array input (the reference returns numpy arrays)."""
+    return t if torch.is_tensor(template) else t.cpu().numpy()
+
+
+def _square(a, name):
+    if a.dim() != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError(f"{name} must be square, got shape {tuple(a.shape)}")
+    if a.shape[0] < 1:
+        raise ValueError(f"{name} must have order >= 1")
+    if not bool(torch.isfinite(a).all()):
+        raise ValueError(f"{name} contains non-finite entries")
+    return a
+
+
+def invert_dense(a):
+    """Exact inverse with partial pivoting (blocklinalg.py:50-87), computed
+    on the device by Gauss-Jordan elimination on [A | I] (psm_invert_dense);
+    the result is column-major like the reference's.  Raises
+    SingularMatrixError when a pivot magnitude drops below 1e-14 ||A||_inf."""
+    src = a
+    t = _square(_device_tensor(a, "invert_dense"), "matrix")
+    n = t.shape[0]
+    # [A | I] column-major: the rows of this (2n, n) C-contiguous tensor are its columns
+    w = torch.empty((2 * n, n), dtype=torch.float64, device=t.device)
+    w[:n].copy_(t.T)
+    w[n:].copy_(torch.eye(n, dtype=torch.float64, device=t.device))
+    work = torch.empty(3 * n + 4, dtype=torch.float64, device=t.device)
+    step, piv = ctypes.c_int(), ctypes.c_double()
+    with torch.cuda.device(t.device):
+        stream = ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+        rc = _lib.load().psm_invert_dense(ctypes.c_void_p(w.data_ptr()), n, ctypes.c_void_p(work.data_ptr()),
+                                          ctypes.byref(step), ctypes.byref(piv), stream)
+    if rc == _lib.PSM_ESINGULAR:
+        if step.value < 0:
+            raise SingularMatrixError("matrix is exactly zero")
+        raise SingularMatrixError(f"pivot {piv.value:.3e} at step {step.value - 1} below 1e-14 * ||A||_inf")
+    _lib.check(rc, "invert_dense")
+    inv = w[n:].T  # (n, n) values, column-major strides
+    return _like_input(inv, src)
+
+
+def matvec(m, x):
+    """y = M x with the fixed ascending-column accumulation order of the
+    reference (blocklinalg.py:90-105): bit-identical, on the device."""
+    return _matvec(m, x, None, 0.0)
+
+
+def _matvec(m, x, u, omega):
+    src = x
+    mt = _device_tensor(m, "matvec")
+    if mt.dim() != 2 or mt.shape[0] != mt.shape[1]:
+        raise ValueError(f"matrix must be square, got shape {tuple(mt.shape)}")
+    n = mt.shape[0]
+    xt = _device_tensor(x, "matvec", mt.device).contiguous()
+    if tuple(xt.shape) != (n,):
+        raise ValueError(f"vector shape {tuple(xt.shape)} does not match order {n}")
+    # column-major storage: column j contiguous
+    mc = mt.T.contiguous()
+    ut = None
+    if u is not None:
+        ut = _device_tensor(u, "block_update", mt.device).contiguous()
+        if tuple(ut.shape) != (n,):
+            raise ValueError(f"block shape {tuple(ut.shape)} does not match order {n}")
+    y = torch.empty(n, dtype=torch.float64, device=mt.device)
+    with torch.cuda.device(mt.device):
+        stream = ctypes.c_void_p(torch.cuda.current_stream(mt.device).cuda_stream)
+        _lib.check(_lib.load().psm_matvec(ctypes.c_void_p(mc.data_ptr()), ctypes.c_void_p(xt.data_ptr()),
+                                          ctypes.c_void_p(ut.data_ptr()) if ut is not None else None,
+                                          float(omega), ctypes.c_void_p(y.data_ptr()), n, stream), "matvec")
+    return _like_input(y, src)
 
 
 def block_kind(extent):

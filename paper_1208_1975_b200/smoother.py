@@ -43,6 +43,7 @@ __all__ = [
     "smooth_chaotic_gs_step",
     "residual_norm",
     "block_shape_of",
+    "block_update",
 ]
 
 SCHEMES = ("block_jacobi", "chaotic_block_gs")
@@ -235,6 +236,15 @@ def smooth_chaotic_gs_step(level, config, cache):
         raise ValueError(f"config.scheme is {config.scheme!r}, not chaotic_block_gs")
     _run(level, config, _Plan(level, config, cache), 1, False, None)
     return level
+
+
+def block_update(u_b, r_b, inv, omega):
+    """One exact block relaxation u_b + omega * (inv @ r_b) as a new vector
+    (smoother.py:90-93): the reference's ascending-column matvec and its two
+    roundings, in one device kernel (psm_matvec); bit-identical."""
+    from .blocklinalg import _matvec
+
+    return _matvec(inv, r_b, u_b, omega)
 
 
 def residual_norm(level, stencil):

@@ -10,24 +10,49 @@ for the multi-patch configuration.
 
 from __future__ import annotations
 
+import itertools
+import os
+
 import numpy as np
 import torch
 
 from .grid import Level, Patch, PatchDims, _int3
 
-__all__ = ["build_level", "build_lattice", "seed_initial_guess", "cells_smoothed"]
+__all__ = ["build_level", "build_lattice", "seed_initial_guess", "cells_smoothed", "allocation_cap"]
 
 
-def build_level(sizes, device=None):
-    """Patches of the given interior sizes abutting along x (bench.py:106-131)."""
+CAP_ENV = "PATCHSMOOTH_MAX_CELLS"  # bench.py:40-41
+DEFAULT_CAP = 300_000_000
+
+
+def allocation_cap():
+    """Cell cap for build_level: $PATCHSMOOTH_MAX_CELLS or 3e8 (bench.py:93-103).
+    The device holds far more (180 GB); raise the variable for big levels."""
+    raw = os.environ.get(CAP_ENV)
+    if raw is None:
+        return DEFAULT_CAP
+    try:
+        cap = int(raw)
+    except ValueError:
+        raise ValueError(f"{CAP_ENV} must be an integer, got {raw!r}") from None
+    if cap < 1:
+        raise ValueError(f"{CAP_ENV} must be positive, got {cap}")
+    return cap
+
+
+def build_level(sizes, max_cells=None, device=None):
+    """Patches of the given interior sizes abutting end to end along x
+    (bench.py:106-131).  Allocation (two padded buffers plus f per patch)
+    must fit ``max_cells`` (default: ``allocation_cap()``)."""
     dims = [PatchDims(*_int3(s, "patch size")) for s in sizes]
     if not dims:
         raise ValueError("no patch sizes given")
-    patches, x0 = [], 0
-    for d in dims:
-        patches.append(Patch(d, origin=(x0, 0, 0), device=device))
-        x0 += d.nx
-    return Level(patches)
+    cap = allocation_cap() if max_cells is None else max_cells
+    need = sum(2 * d.total_cells + d.interior_cells for d in dims)
+    if need > cap:
+        raise ValueError(f"patch set needs {need} cells, cap is {cap} (raise {CAP_ENV} to allow it)")
+    origins = itertools.accumulate([0] + [d.nx for d in dims[:-1]])
+    return Level([Patch(d, origin=(x0, 0, 0), device=device) for d, x0 in zip(dims, origins)])
 
 
 def build_lattice(counts, size, device=None):

@@ -1,4 +1,5 @@
 #!/bin/bash
+export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}  # device-sized levels
 # Round evidence: bench (both arms), per-config timings, launch lists and full
 # ncu captures of the top kernels.  Outputs under gpurun_out/round/.
 O=gpurun_out/round; mkdir -p $O

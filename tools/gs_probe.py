@@ -6,6 +6,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("PATCHSMOOTH_MAX_CELLS", str(10**11))  # device-sized levels
 import torch  # noqa: E402
 
 import paper_1208_1975_b200 as ps  # noqa: E402

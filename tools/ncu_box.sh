@@ -1,4 +1,5 @@
 #!/bin/bash
+export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}  # device-sized levels
 # full ncu capture of one box-block Jacobi sweep: tools/ncu_box.sh N B OUT
 N=${1:-256}; B=${2:-8}; OUT=${3:-prof_box}
 mkdir -p gpurun_out

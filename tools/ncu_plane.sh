@@ -1,4 +1,5 @@
 #!/bin/bash
+export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}  # device-sized levels
 # ncu of the plane-Jacobi kernels at NX^3 (launch list + one full capture of the banded solve)
 NX=${1:-512}; OUT=${2:-prof_plane}
 mkdir -p gpurun_out

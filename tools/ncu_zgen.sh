@@ -1,4 +1,5 @@
 #!/bin/bash
+export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}  # device-sized levels
 # full ncu capture of one runtime-nx line-Jacobi sweep (zgen) on the mixed
 # Table-2 patch set: tools/ncu_zgen.sh OUT
 OUT=${1:-prof_zgen}
