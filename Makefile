@@ -16,7 +16,7 @@ build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/obj/$*.ptxas.log || (cat build/obj/$*.ptxas.log; exit 1)
 
 $(PKG)/libpsmooth.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -Xlinker --no-undefined -o $@ $(OBJS) -lcublas -lcudart
+	$(NVCC) $(ARCH) -shared -Xlinker --no-undefined -o $@ $(OBJS) -lcudart
 	@cat build/obj/*.ptxas.log > build_ptxas.log
 
 oracle:

@@ -18,9 +18,13 @@ Keys beyond the base contract:
                 algorithmic bytes per update (read u, read f, write v) over its
                 CUDA-event duration inside the timed region, vs the measured
                 copy bandwidth in MEASURED_PEAKS.json
+  north_star_512  the BASELINE north-star target: device-timed 512^3
+                line-Jacobi sweep and its fraction of 8 TB/s (N=1 only)
   cpu_baseline  the oracle's C restatement (OpenMP, all host cores) on a
-                bounded slab of the same workload ("port": the reference is pure
-                Python with no native code to build)
+                bounded slab of the same workload ("port"), with
+                ``reference_py``: the reference package itself (patchsmooth
+                from baseline/_ref, serial, its own run_bench) on a smaller
+                slab of the same line length
   e2e           the same metric through the public API with host buffers:
                 per call H2D of u and f from pinned memory, smooth(...) with
                 --e2e-sweeps sweeps including the history, D2H of u + history
@@ -60,6 +64,7 @@ def parse():
     ap.add_argument("--e2e-calls", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -211,6 +216,7 @@ def run_reference(args, rank, world):
     port = CpuPort(nx, ny, 8)
     value, n, el = port.rate(steps=args.steps, warmup=args.warmup)
     cb = port.describe(value, n, el)
+    cb["reference_py"] = _reference_py(nx)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -365,7 +371,10 @@ def run_ours(args, rank, world, local_rank):
         "unit": "GB/s",
         "frac": achieved / peak,
         "traffic": _traffic(f"line_jacobi_{nx}x{ny}x{p.dims.nz}"),
-        "kernel": f"psm::line_jacobi_zmarch_kernel<{nx},1> (line Jacobi sweep, fused residual norm + x ghosts)",
+        "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                          "from the committed ncu --set full capture of this shape (null when none)",
+        "kernel": f"psm::line_jacobi_zmarch_kernel<{nx},1,{2 if halo is not None else 0}> (line Jacobi sweep, fused "
+                  "residual norm + x ghosts" + (", peer-halo stores)" if halo is not None else ")"),
         "bytes_per_launch": BYTES_PER_UPDATE * local_cells,
         "avg_launch_ms": sweep_ms,
         "peak_source": peak_src,
@@ -378,11 +387,19 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         e2e = _e2e(args, dom, cfg, cache, dev, world, rank)
 
+    # ---- the north-star grid: 512^3 line-Jacobi sweep, device-timed --------
+    north = None
+    if world == 1 and not args.no_north_star:
+        del dom, p, plan, dp
+        torch.cuda.empty_cache()
+        north = _north_star(args, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         port = CpuPort(nx, ny, 8)
         v, n, el = port.rate(seconds=args.cpu_seconds)
         cpu = port.describe(v, n, el)
+        cpu["reference_py"] = _reference_py(nx)
 
     if rank == 0:
         line = {
@@ -409,15 +426,113 @@ def run_ours(args, rank, world, local_rank):
                     " + halo fused into the sweep (peer-memory stores, step flags)" if halo is not None else
                     " + NCCL halo, overlapped"),
                 "halo": None if world == 1 else halo_mode,
-                "l2": "no flush: inputs 25.8 GB per sweep >> 126 MB L2",
+                "l2": f"no flush: inputs {BYTES_PER_UPDATE * local_cells / 1e9:.1f} GB per sweep per GPU "
+                      ">> 126 MB L2",
             },
             "roofline": roofline,
+            "north_star_512": north,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+
+
+def _north_star(args, dev, n=512, sweeps=20):
+    """The north-star target (BASELINE.json): one 512^3 line-Jacobi sweep on
+    one B200, >= 70% of the 8 TB/s HBM roofline.  Timed like the headline:
+    CUDA events around each sweep launch on the launching stream, after
+    warm-up; inputs (3.2 GB per sweep) far exceed L2."""
+    import torch
+
+    import paper_1208_1975_b200 as ps
+    from paper_1208_1975_b200 import _lib
+    from paper_1208_1975_b200.dist import SlabDomain
+    from paper_1208_1975_b200.smoother import _Plan
+
+    dom = SlabDomain((n, n, n), 0, 1, device=dev)
+    p = dom.patch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(512)
+    p.interior.copy_(torch.rand(p.interior.shape, generator=gen, device=dev, dtype=torch.float64))
+    p.f.copy_(torch.randn(p.f.shape, generator=gen, device=dev, dtype=torch.float64))
+    cfg = ps.SmootherConfig(scheme="block_jacobi", block_dims=(n, 1, 1), omega=0.8, steps=1,
+                            strategy=ps.ExecutionStrategy.device())
+    dp = _Plan(dom.level, cfg, ps.InverseCache()).dev
+    dp.reserve(2)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(dev)
+    act = (ctypes.c_ubyte * 1)()
+    dp.refresh(_lib.GHOST_ALL)
+    pairs = []
+    for s in range(args.warmup + sweeps):
+        act[0] = p._active
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(lib.psm_jacobi_sweep(dp.handle, act, 0.8, s % 2, ctypes.c_void_p(stream.cuda_stream)),
+                   "jacobi_sweep")
+        e1.record(stream)
+        if s >= args.warmup:
+            pairs.append((e0, e1))
+        p.swap_buffers()
+        dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
+    torch.cuda.synchronize(dev)
+    ms = sorted(a.elapsed_time(b) for a, b in pairs)
+    avg = sum(ms) / len(ms)
+    cells = n ** 3
+    gbs = BYTES_PER_UPDATE * cells / (avg / 1e3) / 1e9
+    peak, src = _peaks()
+    out = {
+        "workload": f"{n}^3 single patch, line block Jacobi (block_dims ({n},1,1), omega 0.8), 1 GPU",
+        "kernel": f"psm::line_jacobi_zmarch_kernel<{n},1,0>",
+        "sweeps": sweeps,
+        "avg_sweep_ms": avg,
+        "median_sweep_ms": ms[len(ms) // 2],
+        "Gupdates_per_s": cells / (avg / 1e3) / 1e9,
+        "achieved_GBps": gbs,
+        "frac_of_nominal_8000": gbs / 8000.0,
+        "frac_of_measured": gbs / peak,
+        "peak_source": src,
+        "target": ">= 0.70 of 8 TB/s",
+    }
+    del dom, p, dp
+    torch.cuda.empty_cache()
+    return out
+
+
+def _reference_py(nx, ny=16, nz=8, repeat=2):
+    """The reference smoother itself (patchsmooth, pure Python/numpy, from
+    baseline/_ref, installed by __graft_entry__.build()) on a bounded slab of
+    the workload, through its own harness: build_level, seed_initial_guess,
+    run_bench (warm inverse cache, min of `repeat` smooth() calls incl.
+    ghosts and history), serial strategy (its fastest: SURVEY F7)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "patchsmooth")):
+        return {"unavailable": "baseline/_ref/patchsmooth not installed (run __graft_entry__.build() where "
+                               "/root/reference exists)"}
+    sys.path.insert(0, ref)
+    try:
+        import patchsmooth as R
+    finally:
+        sys.path.remove(ref)
+    level = R.build_level([(nx, ny, nz)])
+    R.seed_initial_guess(level, 42)
+    cfg = R.SmootherConfig(scheme="block_jacobi", block_dims=(nx, 1, 1), steps=1)
+    t0 = time.perf_counter()
+    rec = R.run_bench(level, [cfg], repeat=repeat, label=f"{nx}x{ny}x{nz}")[0]
+    total = time.perf_counter() - t0
+    return {
+        "value": rec.cells_per_second / 1e9,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "reference",
+        "sample": f"patchsmooth {getattr(R, '__version__', '?')} run_bench: min of {repeat} smooth() calls "
+                  f"(1 line-Jacobi step + ghosts + 2 history norms) on a {nx}x{ny}x{nz} slab, serial strategy, "
+                  f"inverse cache warmed outside the timing ({total:.1f} s in all)",
+        "wall_seconds": rec.wall_seconds,
+        "host_cpus": os.cpu_count(),
+    }
 
 
 def _e2e(args, dom, cfg, cache, dev, world, rank):

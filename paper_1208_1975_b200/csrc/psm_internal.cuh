@@ -55,6 +55,7 @@ struct PlaneFac {
   int nx, ny;
   double fy_lo, fy_up;
   const double* Q;     // nx*nx orthonormal DST-I basis, symmetric
+  const double* Qf;    // parity-split basis in DMMA fragment order (psm_plane_dst.cu)
   const double* cp;    // [mode][ny] Thomas factors
   const double* invm;  // [mode][ny]
   // banded factorised form (psm_plane_band.cu); bw == 0: not available

@@ -11,10 +11,10 @@
 // x by the orthonormal DST-I basis Q (Q = Q^T = Q^-1).  Per x-mode i the
 // remaining operator is tridiagonal in y with diagonal c + 2a cos(pi i/(nx+1)).
 // So Ainv r = Q * T_i^-1 * (Q r): a GEMM with Q along x, one Thomas solve
-// along y per (plane, mode), and a GEMM back.  The two transforms are plain
-// dense fp64 GEMMs (cuBLAS DGEMM, tensor-core DMMA on sm_100a); the residual,
-// the modal Thomas solves and the relaxation are this file's kernels.
-#include <cublas_v2.h>
+// along y per (plane, mode), and a GEMM back.  The two transforms are the
+// hand-written DMMA tile kernels of psm_plane_dst.cu (parity-split DST-I,
+// residual / relaxation fused into their prologue / epilogue); the modal
+// Thomas solves are this file's kernels.
 #include <math.h>
 #include <string.h>
 
@@ -31,6 +31,16 @@ int band_k_for(int nx);
 cudaError_t launch_plane_band_jacobi(int K, int BW, const PatchDev* patches, const unsigned char* active,
                                      double omega, const double* rbuf, double* zbuf, const int2* units,
                                      int nunits, const double* hinf_host, cudaStream_t s);
+void dst_split_table(const std::vector<double>& Q, int nx, std::vector<double>& out);
+size_t dst_table_doubles(int nx);
+int dst_max_nx();
+cudaError_t launch_dst_rows(int pro, int epi, const PatchDev* patches, int p0, int p1, long long c0, long long nrows,
+                            int nx, const double* qf, const unsigned char* active, const StencilDev& st,
+                            double omega, const double* in, double* out, cudaStream_t s);
+cudaError_t launch_plane_gs_chain(const PlaneFac* d_fac, int nx, const PatchDev* patches, int p0, int np, int maxnz,
+                                  double czw, double* buf, cudaStream_t s);
+enum { kDstProRows = 0, kDstProResidual = 1 };
+enum { kDstEpiStore = 0, kDstEpiRelaxInPlace = 1, kDstEpiRelaxInto = 2 };
 cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
                               const StencilDev& st, double omega, double* partials, double* rbuf, long long tile_base,
                               long long ntiles, int threads, size_t smem, cudaStream_t stream);
@@ -199,150 +209,6 @@ static void launch_modal_thomas(const PlaneFac& h, const PlaneFac* d, double* bu
   }
 }
 
-// Plane GS in the transformed domain, stage k (symmetric y faces).  With
-// rhat = Q r (DST-I along x; Q = Q^T = Q^-1) and the exact plane inverse
-// x = Q S(Q r) (S: the modal y-solves), stage k's residual is the pre-sweep
-// residual minus zm * omega * x(k-1) at the same (x, y), so
-//   rhat(k) = rhat_pre(k) - zm omega xhat(k-1),   xhat(k) = S(rhat(k)),
-// and no transform runs inside the stage loop: one DGEMM transforms every
-// plane's pre-sweep residual before it, one transforms every xhat back after
-// it.  Thread pair per (patch, mode) as plane_modal_thomas2_kernel; planes
-// of patches p0.. at their own offsets in `buf` (cell-major, cell0).
-__global__ void plane_gs_stage_kernel(const PlaneFac* __restrict__ F, const PatchDev* __restrict__ patches, int p0,
-                                      long long nplanes, int k, double czw, double* __restrict__ buf) {
-  constexpr int B = 16;
-  const int nx = F->nx, ny = F->ny, m = ny / 2;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool in = t < 2 * nplanes * nx;
-  const long long line = in ? t >> 1 : 0;
-  const int bot = (int)(t & 1);
-  const long long pl = line / nx;
-  const int i = (int)(line - pl * nx);
-  const long long plane_cells = (long long)nx * ny;
-  double* b = buf + patches[p0 + pl].cell0 + (long long)k * plane_cells + i;
-  const double* bp = b - plane_cells;  // xhat(k-1) of the same patch (k > 0)
-  const double* cp = F->cp + i;
-  const double* invm = F->invm + i;
-  const double lo = F->fy_lo;
-  const int len = bot ? ny - m : m;
-  const long long j0 = bot ? ny - 1 : 0, dj = bot ? -nx : nx;
-  // warm L2 with this patch's next plane while the stage runs (the next
-  // stage's loads then come from L2, not HBM)
-  // (bulk prefetches need a 16-byte aligned address and size; cell0 offsets
-  // of earlier odd-sized patches can leave the plane only 8-byte aligned)
-  if (in && i == 0 && bot == 0 && k + 1 < patches[p0 + pl].nz && ((plane_cells * 8) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(b + plane_cells) & 15) == 0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b + plane_cells), "r"((unsigned)(plane_cells * 8))
-                 : "memory");
-  double prev = 0.0;
-  int jj = 0;
-  if (in) {
-    for (; jj + B <= len; jj += B) {
-      double v[B], mm[B];
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        v[q] = b[j0 * nx + (jj + q) * dj];
-        if (k > 0) v[q] = fma(-czw, bp[j0 * nx + (jj + q) * dj], v[q]);
-        mm[q] = __ldg(invm + (long long)(jj + q) * nx);
-      }
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        prev = fma(-lo, prev, v[q]) * mm[q];
-        b[j0 * nx + (jj + q) * dj] = prev;
-      }
-    }
-    for (; jj < len; ++jj) {
-      double v = b[j0 * nx + jj * dj];
-      if (k > 0) v = fma(-czw, bp[j0 * nx + jj * dj], v);
-      prev = fma(-lo, prev, v) * invm[(long long)jj * nx];
-      b[j0 * nx + jj * dj] = prev;
-    }
-  }
-  const double c_own = in && len > 0 ? __ldg(cp + (long long)(len - 1) * nx) : 0.0;
-  const double y_oth = __shfl_xor_sync(0xffffffffu, prev, 1);
-  const double c_oth = __shfl_xor_sync(0xffffffffu, c_own, 1);
-  const double yT = bot ? y_oth : prev, yB = bot ? prev : y_oth;
-  const double cT = bot ? c_oth : c_own, cB = bot ? c_own : c_oth;
-  const double xT = (yT - cT * yB) / (1.0 - cT * cB);
-  double next = bot ? yB - cB * xT : xT;
-  if (!in || len == 0) return;
-  b[j0 * nx + (len - 1) * dj] = next;
-  jj = len - 2;
-  for (; jj - B + 1 >= 0; jj -= B) {
-    double v[B], c[B];
-#pragma unroll
-    for (int q = 0; q < B; ++q) {
-      v[q] = b[j0 * nx + (jj - q) * dj];
-      c[q] = __ldg(cp + (long long)(jj - q) * nx);
-    }
-#pragma unroll
-    for (int q = 0; q < B; ++q) {
-      next = fma(-c[q], next, v[q]);
-      b[j0 * nx + (jj - q) * dj] = next;
-    }
-  }
-  for (; jj >= 0; --jj) {
-    next = fma(-cp[(long long)jj * nx], next, b[j0 * nx + jj * dj]);
-    b[j0 * nx + jj * dj] = next;
-  }
-}
-
-// GS epilogue: u += omega * x in place for every interior cell (the
-// refresh after a GS sweep fills all physical ghosts)
-__global__ void plane_relax_inplace_kernel(const PatchDev* __restrict__ patches, int npatch,
-                                           const unsigned char* __restrict__ active, double omega,
-                                           const double* __restrict__ xbuf, long long total, long long first) {
-  for (long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; g0 < total;
-       g0 += (long long)gridDim.x * blockDim.x) {
-    const long long g = g0 + first;
-    int lo = 0, hi = npatch - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (patches[mid].cell0 <= g) lo = mid; else hi = mid - 1;
-    }
-    const PatchDev& P = patches[lo];
-    const long long e = g - P.cell0;
-    const int nx = P.nx, ny = P.ny;
-    const long long row = e / nx;
-    const int x = (int)(e - row * nx);
-    const int k = (int)(row / ny), j = (int)(row - (long long)k * ny);
-    const long long px = nx + 2, pxy = px * (ny + 2);
-    double* u = P.buf[active[lo]];
-    const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
-    u[iu] = relax(u[iu], omega, xbuf[g0]);
-  }
-}
-
-// Jacobi epilogue: v = u + omega * x for every interior cell, plus the
-// physical x-face ghosts of v (fused, see psm_line.cu).
-__global__ void plane_relax_kernel(const PatchDev* __restrict__ patches, int npatch,
-                                   const unsigned char* __restrict__ active, double omega,
-                                   const double* __restrict__ xbuf, long long total, long long first) {
-  for (long long g0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; g0 < total;
-       g0 += (long long)gridDim.x * blockDim.x) {
-    const long long g = g0 + first;  // cells [first, first + total); xbuf starts at cell `first`
-    int lo = 0, hi = npatch - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (patches[mid].cell0 <= g) lo = mid; else hi = mid - 1;
-    }
-    const PatchDev& P = patches[lo];
-    const long long e = g - P.cell0;
-    const int nx = P.nx, ny = P.ny;
-    const long long row = e / nx;
-    const int x = (int)(e - row * nx);
-    const int k = (int)(row / ny), j = (int)(row - (long long)k * ny);
-    const long long px = nx + 2, pxy = px * (ny + 2);
-    const int act = active[lo];
-    const long long iu = (long long)(k + 1) * pxy + (long long)(j + 1) * px + x + 1;
-    const double nv = relax(P.buf[act][iu], omega, xbuf[g0]);
-    double* v = P.buf[act ^ 1];
-    v[iu] = nv;
-    if (x == 0) v[iu - 1] = -nv;
-    if (x == nx - 1) v[iu + 1] = -nv;
-  }
-}
-
 // GS stage k epilogue fused with stage k+1's residual: u(k) += omega x in
 // place, then r(k+1) = f - A u at the same (x, y), which reads u(k) only at
 // this cell (its z-neighbour, just updated by this thread) and plane k+1's
@@ -391,6 +257,7 @@ struct PlaneRun {  // consecutive patches sharing one PlaneFac (same nx, ny)
   const PlaneFac* d_fac;
   const PlaneFac* h_fac;
   const double* Q;
+  const double* Qf;  // split DST table (psm_plane_dst.cu)
   int nx, ny;
   int bw = 0;              // banded factorised solve available (psm_plane_band.cu)
   int2* d_units = nullptr;  // (patch, plane) units of the run for the banded kernel
@@ -399,10 +266,7 @@ struct PlaneRun {  // consecutive patches sharing one PlaneFac (same nx, ny)
 };
 int psm_plane_band_mode = -1;  // -1: auto (banded where available), 0: DST only (tests/bench)
 
-constexpr size_t kBlasWs = 32u << 20;
 struct PlaneState {
-  cublasHandle_t handle = nullptr;
-  void* blas_ws = nullptr;
   double* rbuf = nullptr;   // sum of cells: residual, then x
   double* rhat = nullptr;   // sum of cells: modal coefficients
   double* sbuf = nullptr;   // GS stage buffers (sum over patches of nx*ny), x2
@@ -427,11 +291,6 @@ extern "C" cudaError_t psm_side_join(psm_plan* P, cudaStream_t s, int n);
   do {                                                                                   \
     cudaError_t _e = (expr);                                                             \
     if (_e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(_e));      \
-  } while (0)
-#define PBLAS(expr)                                                                      \
-  do {                                                                                   \
-    cublasStatus_t _s = (expr);                                                          \
-    if (_s != CUBLAS_STATUS_SUCCESS) return psm_set_error(PSM_ECUDA, "cuBLAS call failed: " #expr); \
   } while (0)
 
 int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
@@ -462,7 +321,9 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
   int bw = 0, nj = 0;
   std::vector<double> band;
   plane_band_tables(c, a, ylo, yup, nx, ny, &bw, &nj, band);
-  const size_t bytes = sizeof(PlaneFac) + (nq + 2 * nt + band.size()) * sizeof(double);
+  std::vector<double> qf;
+  if (nx <= dst_max_nx()) dst_split_table(Q, nx, qf);
+  const size_t bytes = sizeof(PlaneFac) + (nq + 2 * nt + band.size() + qf.size()) * sizeof(double);
   if (cudaMalloc(&F->dev, bytes) != cudaSuccess) return psm_set_error(PSM_ENOMEM, "cudaMalloc for plane factors");
   double* tab = (double*)((char*)F->dev + sizeof(PlaneFac));
   PlaneFac& H = F->h_plane;
@@ -477,6 +338,7 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
   H.bw = bw;
   H.nj = nj;
   H.H = band.empty() ? nullptr : tab + nq + 2 * nt;
+  H.Qf = qf.empty() ? nullptr : tab + nq + 2 * nt + band.size();
   F->d_plane = (PlaneFac*)F->dev;
   PCUDA(cudaMemcpy(F->dev, &H, sizeof H, cudaMemcpyHostToDevice));
   PCUDA(cudaMemcpy(tab, Q.data(), nq * sizeof(double), cudaMemcpyHostToDevice));
@@ -484,20 +346,20 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
   PCUDA(cudaMemcpy(tab + nq + nt, invm.data(), nt * sizeof(double), cudaMemcpyHostToDevice));
   if (!band.empty())
     PCUDA(cudaMemcpy(tab + nq + 2 * nt, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (!qf.empty())
+    PCUDA(cudaMemcpy(tab + nq + 2 * nt + band.size(), qf.data(), qf.size() * sizeof(double),
+                     cudaMemcpyHostToDevice));
   return PSM_OK;
 }
 
-// out = Q_x applied to `nvec` row-major vectors of length nx stored with
-// leading dimension nx: in column-major terms out(nx x nvec) = Q * in.
-static int dst_gemm(cublasHandle_t h, const double* Q, int nx, const double* in, double* out, long long nvec) {
-  const double one = 1.0, zero = 0.0;
-  // split huge batches so n fits an int
-  const long long maxn = 1LL << 30;
-  for (long long off = 0; off < nvec; off += maxn) {
-    const int n = (int)std::min(maxn, nvec - off);
-    PBLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, nx, n, nx, &one, Q, nx, in + off * nx, nx, &zero,
-                      out + off * nx, nx));
-  }
+// out = Q_x applied to `nvec` row-major vectors of length nx (the DMMA tile
+// kernel of psm_plane_dst.cu, no fusion)
+static int dst_rows(const PlaneFac& h, const double* in, double* out, long long nvec, cudaStream_t s) {
+  if (!h.Qf)
+    return psm_set_error(PSM_EUNSUPPORTED, "DST plane transforms support nx <= 512 (use the banded plane solver)");
+  static const StencilDev none{};
+  PCUDA(launch_dst_rows(kDstProRows, kDstEpiStore, nullptr, 0, 0, 0, nvec, h.nx, h.Qf, nullptr, none, 0.0, in, out,
+                        s));
   return PSM_OK;
 }
 
@@ -508,27 +370,18 @@ int psm_plane_apply(const psm_factors* F, const double* r, double* x, long long 
   if (n == 0) return PSM_OK;
   double* tmp = nullptr;
   PCUDA(cudaMallocAsync(&tmp, n * sizeof(double), stream));
-  cublasHandle_t h;
-  PBLAS(cublasCreate(&h));
-  cublasSetStream(h, stream);
-  int rc = dst_gemm(h, H.Q, H.nx, r, tmp, (long long)H.ny * count);
+  int rc = dst_rows(H, r, tmp, (long long)H.ny * count, stream);
   if (rc == PSM_OK) {
     launch_modal_thomas(H, F->d_plane, tmp, count, stream);
-    rc = dst_gemm(h, H.Q, H.nx, tmp, x, (long long)H.ny * count);
+    rc = dst_rows(H, tmp, x, (long long)H.ny * count, stream);
   }
   cudaFreeAsync(tmp, stream);
-  cudaStreamSynchronize(stream);
-  cublasDestroy(h);
   return rc;
 }
 
 int psm_plane_plan_setup(psm_plan* P) {
   PlaneState* S = new PlaneState();
   P->plane = S;
-  PBLAS(cublasCreate(&S->handle));
-  // explicit workspace: cuBLAS must not allocate while a CUDA graph captures
-  PCUDA(cudaMalloc(&S->blas_ws, kBlasWs));
-  PBLAS(cublasSetWorkspace(S->handle, S->blas_ws, kBlasWs));
   long long cells = 0;
   for (auto& h : P->hp) cells += (long long)h.nx * h.ny * h.nz;
   PCUDA(cudaMalloc(&S->rbuf, cells * sizeof(double)));
@@ -555,6 +408,7 @@ int psm_plane_plan_setup(psm_plan* P) {
     r.d_fac = P->fac[p]->d_plane;
     r.h_fac = &P->fac[p]->h_plane;
     r.Q = P->fac[p]->h_plane.Q;
+    r.Qf = P->fac[p]->h_plane.Qf;
     r.nx = P->hp[p].nx;
     r.ny = P->hp[p].ny;
     r.bw = P->fac[p]->h_plane.bw;
@@ -582,8 +436,6 @@ int psm_plane_plan_setup(psm_plan* P) {
 int psm_plane_plan_free(psm_plan* P) {
   PlaneState* S = P->plane;
   if (!S) return PSM_OK;
-  if (S->handle) cublasDestroy(S->handle);
-  cudaFree(S->blas_ws);
   cudaFree(S->rbuf);
   cudaFree(S->rhat);
   cudaFree(S->sbuf);
@@ -606,7 +458,6 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
     const int rc = psm_plane_residual(P, da, partials, S->rbuf, s);
     if (rc) return rc;
   }
-  cublasSetStream(S->handle, s);
   // banded runs: several at once on side streams when there are several
   int nband = 0;
   for (const PlaneRun& r : S->runs) nband += (r.bw > 0 && psm_plane_band_mode != 0);
@@ -627,17 +478,17 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
       P->launches += 1;
       continue;
     }
+    // DST -> modal Thomas -> DST back with v = u + omega x (and v's x
+    // ghosts) in the back transform's epilogue
     const long long nvec = planes * r.ny;
-    int rc = dst_gemm(S->handle, r.Q, r.nx, S->rbuf + c0, S->rhat + c0, nvec);
+    (void)cells;
+    const int rc = dst_rows(*r.h_fac, S->rbuf + c0, S->rhat + c0, nvec, s);
     if (rc) return rc;
     launch_modal_thomas(*r.h_fac, r.d_fac, S->rhat + c0, planes, s);
     PCUDA(cudaGetLastError());
-    rc = dst_gemm(S->handle, r.Q, r.nx, S->rhat + c0, S->rbuf + c0, nvec);
-    if (rc) return rc;
-    plane_relax_kernel<<<blocks_for(cells, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega, S->rbuf + c0,
-                                                              cells, c0);
-    PCUDA(cudaGetLastError());
-    P->launches += 4;
+    PCUDA(launch_dst_rows(kDstProRows, kDstEpiRelaxInto, P->d_patches, r.p0, r.p1, c0, nvec, r.nx, r.Qf, da, P->st,
+                          omega, S->rhat + c0, nullptr, s));
+    P->launches += 3;
   }
   if (fan) PCUDA(psm_side_join(P, s, nband));
   return PSM_OK;
@@ -655,51 +506,26 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
   bool sym = !getenv("PSM_PLANE_GS_STAGED");
   for (const PlaneRun& r : S->runs) sym = sym && r.h_fac->fy_lo == r.h_fac->fy_up;
   if (!sym) return psm_plane_gs_staged(P, da, omega, s);
-  {
-    const int rc = psm_plane_residual(P, da, P->d_scratch, S->rbuf, s);
-    if (rc) return rc;
-  }
-  cublasSetStream(S->handle, s);
-  int maxnz = 0;
-  for (auto& h : P->hp) maxnz = std::max(maxnz, h.nz);
+  for (const PlaneRun& r : S->runs)
+    if (!r.Qf) return psm_set_error(PSM_EUNSUPPORTED, "plane GS supports nx <= 512");
+  const double czw = P->st.zm * omega;
   for (const PlaneRun& r : S->runs) {
     const long long c0 = P->hp[r.p0].cell0;
     long long planes = 0;
-    for (int p = r.p0; p < r.p1; ++p) planes += P->hp[p].nz;
-    const int rc = dst_gemm(S->handle, r.Q, r.nx, S->rbuf + c0, S->rhat + c0, planes * r.ny);
-    if (rc) return rc;
-    P->launches += 1;
-  }
-  const double czw = P->st.zm * omega;
-  for (int k = 0; k < maxnz; ++k) {
-    for (const PlaneRun& r : S->runs) {
-      int p0 = r.p0;
-      while (p0 < r.p1) {
-        if (k >= P->hp[p0].nz) { ++p0; continue; }
-        int p1 = p0 + 1;
-        while (p1 < r.p1 && k < P->hp[p1].nz) ++p1;
-        const long long nplanes = p1 - p0;
-        plane_gs_stage_kernel<<<(unsigned)((2 * nplanes * r.nx + 127) / 128), 128, 0, s>>>(
-            r.d_fac, P->d_patches, p0, nplanes, k, czw, S->rhat);
-        PCUDA(cudaGetLastError());
-        P->launches += 1;
-        p0 = p1;
-      }
-    }
-  }
-  for (const PlaneRun& r : S->runs) {
-    const long long c0 = P->hp[r.p0].cell0;
-    long long planes = 0, cells = 0;
+    int maxnz = 0;
     for (int p = r.p0; p < r.p1; ++p) {
       planes += P->hp[p].nz;
-      cells += (long long)P->hp[p].nx * P->hp[p].ny * P->hp[p].nz;
+      maxnz = std::max(maxnz, P->hp[p].nz);
     }
-    const int rc = dst_gemm(S->handle, r.Q, r.nx, S->rhat + c0, S->rbuf + c0, planes * r.ny);
-    if (rc) return rc;
-    plane_relax_inplace_kernel<<<blocks_for(cells, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, omega,
-                                                                      S->rbuf + c0, cells, c0);
-    PCUDA(cudaGetLastError());
-    P->launches += 2;
+    // 1. rhat = Q r_pre: the pre-sweep residual of every row, transformed
+    PCUDA(launch_dst_rows(kDstProResidual, kDstEpiStore, P->d_patches, r.p0, r.p1, c0, planes * r.ny, r.nx, r.Qf, da,
+                          P->st, 0.0, nullptr, S->rhat + c0, s));
+    // 2. every (patch, mode) chain over the stages k, one launch
+    PCUDA(launch_plane_gs_chain(r.d_fac, r.nx, P->d_patches, r.p0, r.p1 - r.p0, maxnz, czw, S->rhat + c0, s));
+    // 3. x = Q xhat, relaxed into u in place
+    PCUDA(launch_dst_rows(kDstProRows, kDstEpiRelaxInPlace, P->d_patches, r.p0, r.p1, c0, planes * r.ny, r.nx, r.Qf,
+                          da, P->st, omega, S->rhat + c0, nullptr, s));
+    P->launches += 3;
   }
   return PSM_OK;
 }
@@ -708,7 +534,6 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
 // relax in place fused with the next stage's residual.
 static int psm_plane_gs_staged(psm_plan* P, const unsigned char* da, double omega, cudaStream_t s) {
   PlaneState* S = P->plane;
-  cublasSetStream(S->handle, s);
   int maxnz = 0;
   for (auto& h : P->hp) maxnz = std::max(maxnz, h.nz);
   plane_stage_residual_kernel<<<blocks_for(S->stage_total, 256), 256, 0, s>>>(P->d_patches, P->npatch, da, P->st, 0,
@@ -725,11 +550,11 @@ static int psm_plane_gs_staged(psm_plan* P, const unsigned char* da, double omeg
         while (p1 < r.p1 && k < P->hp[p1].nz) ++p1;
         const long long o = S->stage_off[p0];
         const long long nplanes = p1 - p0;
-        int rc = dst_gemm(S->handle, r.Q, r.nx, S->sbuf + o, S->shat + o, nplanes * r.ny);
+        int rc = dst_rows(*r.h_fac, S->sbuf + o, S->shat + o, nplanes * r.ny, s);
         if (rc) return rc;
         launch_modal_thomas(*r.h_fac, r.d_fac, S->shat + o, nplanes, s);
         PCUDA(cudaGetLastError());
-        rc = dst_gemm(S->handle, r.Q, r.nx, S->shat + o, S->sbuf + o, nplanes * r.ny);
+        rc = dst_rows(*r.h_fac, S->shat + o, S->sbuf + o, nplanes * r.ny, s);
         if (rc) return rc;
         P->launches += 3;
         p0 = p1;
