@@ -300,13 +300,17 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     nstep = [0]  # p2p: steps since the halo's epoch
 
+    halo_waits = []  # N > 1: per step, the event pair around this rank's halo stall
+
     def step(s, record):
         # the sweep launches are bracketed by events on the launching stream
         if halo is not None:
-            jacobi_step_p2p(dom, dp, cfg.omega, s % 2, halo, nstep[0], events=multi_sweeps if record else None)
+            jacobi_step_p2p(dom, dp, cfg.omega, s % 2, halo, nstep[0], events=multi_sweeps if record else None,
+                            waits=halo_waits if record else None)
             nstep[0] += 1
         elif world > 1:
-            jacobi_step_overlapped(dom, dp, cfg.omega, s % 2, events=multi_sweeps if record else None)
+            jacobi_step_overlapped(dom, dp, cfg.omega, s % 2, events=multi_sweeps if record else None,
+                                   waits=halo_waits if record else None)
         else:
             _single_step(s)
 
@@ -363,6 +367,21 @@ def run_ours(args, rank, world, local_rank):
         sweep_ms = sum(sum(a.elapsed_time(b) for a, b in st) for st in multi_sweeps) / len(multi_sweeps)
     local_cells = p.dims.interior_cells
     achieved = BYTES_PER_UPDATE * local_cells / (sweep_ms / 1e3) / 1e9
+    halo_stall = None
+    if world > 1:
+        # this rank's average stall per step waiting for its neighbours'
+        # planes (fused: the flag wait; NCCL: the exchange + unpack), then
+        # every rank's value gathered: overlap shows as a small fraction of
+        # the step
+        mine = sum(a.elapsed_time(b) for a, b in halo_waits) / max(1, len(halo_waits))
+        allw = torch.zeros(world, dtype=torch.float64, device=dev)
+        allw[rank] = mine
+        dist.all_reduce(allw)
+        per = [float(v) for v in allw.cpu()]
+        halo_stall = {"ms_per_step_by_rank": per, "max": max(per), "mean": sum(per) / world,
+                      "frac_of_step": max(per) / (ms_total / args.steps),
+                      "what": "flag wait kernel (fused peer halo)" if halo is not None else
+                              "stream wait on the NCCL exchange + unpack"}
     peak, peak_src = _peaks()
     roofline = {
         "bound": "hbm",
@@ -431,6 +450,7 @@ def run_ours(args, rank, world, local_rank):
             },
             "roofline": roofline,
             "north_star_512": north,
+            "halo_stall": halo_stall,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -101,6 +101,9 @@ extern int psm_plane_band_mode;  // psm_plane.cu
 bool gs_pipe_supported(int nx);
 int psm_gs_pipe_prepare(psm_plan* P, int* n_tickets);
 void psm_gs_pipe_free(psm_plan* P);
+bool psm_gs_pipe_multi_ok(const psm_plan* P);
+int psm_gs_pipe_multi(psm_plan* P, const unsigned char* da, double omega, int chaotic, int steps, double* hist,
+                      long long hist_stride, int* flags, int* tickets, cudaStream_t s);
 int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int chaotic, int* flags, int* tickets,
                       cudaStream_t s);
 
@@ -508,6 +511,7 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_unit_patch);
   cudaFree(P->d_unit_plane);
   cudaFree(P->d_gsflags);
+  cudaFree(P->d_msflags);
   cudaFree(P->d_boxes);
   cudaFree(P->d_box_regions);
   psm_gs_pipe_free(P);
@@ -1070,6 +1074,51 @@ long long psm_plan_launches(const psm_plan* P) { return P ? P->launches : -1; }
 // history slot, all patches swap, refresh with the x faces skipped) [, final
 // residual]; GS: [refresh, residual] then steps x (sweep, refresh [,
 // residual]).  `act` is updated to the active flags after the steps.
+// Line GS on one patch with physical faces: several steps per launch (the
+// multi-sweep mode of the pipelined kernel, psm_line_gs_pipe.cu); 0 when the
+// plan does not qualify (the caller then runs step by step)
+static int gs_multi_steps(psm_plan* P, const unsigned char* active, double omega, int gs_mode, int steps,
+                          int history, cudaStream_t s, int* done) {
+  *done = 0;
+  if (P->kind != PSM_BLOCK_LINE || steps < 2 || steps >= 0x7fff) return PSM_OK;
+  const char* env = getenv("PSM_GS_MULTI");
+  if (env && env[0] == '0') return PSM_OK;
+  for (auto& h : P->hp)
+    if (!gs_pipe_supported(h.nx) || (((uintptr_t)h.buf[0] | (uintptr_t)h.buf[1]) % 16) != 0) return PSM_OK;
+  if (P->npatch != 1 || P->ncopy != 0) return PSM_OK;
+  if (!P->gspipe) {
+    int nt = 0;
+    int rc = psm_gs_pipe_prepare(P, &nt);
+    if (rc) return rc;
+    P->gs_ntickets = nt;
+    CUDA_TRY(cudaMalloc(&P->d_gsflags, (P->nplanes + nt) * sizeof(int)));
+  }
+  if (!psm_gs_pipe_multi_ok(P)) return PSM_OK;
+  unsigned char* da;
+  int rc = get_active(P, active, &da);
+  if (rc) return rc;
+  // per-sweep progress words (steps * nplanes) and the tickets
+  const long long nflags = (long long)steps * P->nplanes + P->gs_ntickets;
+  if (nflags > P->ms_flag_cap) {
+    if (P->d_msflags) cudaFree(P->d_msflags);
+    P->d_msflags = nullptr;
+    CUDA_TRY(cudaMalloc(&P->d_msflags, nflags * sizeof(int)));
+    P->ms_flag_cap = nflags;
+  }
+  CUDA_TRY(cudaMemsetAsync(P->d_msflags, 0, nflags * sizeof(int), s));
+  double* hist = nullptr;
+  if (history) {
+    hist = slot_ptr(P, 1, &rc);
+    if (rc) return rc;
+  }
+  rc = psm_gs_pipe_multi(P, da, omega, gs_mode == PSM_GS_CHAOTIC, steps, hist, std::max<long long>(1, P->ntiles),
+                         P->d_msflags, P->d_msflags + (long long)steps * P->nplanes, s);
+  if (rc) return rc;
+  P->phys_pending = 2;  // every physical ghost is left to the refresh
+  *done = 1;
+  return PSM_OK;
+}
+
 static int smooth_sequence(psm_plan* P, std::vector<unsigned char>& act, int scheme, double omega, int steps,
                            int gs_mode, int history, void* stream) {
   int rc;
@@ -1091,6 +1140,16 @@ static int smooth_sequence(psm_plan* P, std::vector<unsigned char>& act, int sch
   if (history) {
     rc = psm_residual(P, act.data(), 0, stream);
     if (rc) return rc;
+  }
+  {
+    int done = 0;
+    rc = gs_multi_steps(P, act.data(), omega, gs_mode, steps, history, (cudaStream_t)stream, &done);
+    if (rc) return rc;
+    if (done) {
+      rc = psm_refresh_ghosts(P, act.data(), PSM_GHOST_ALL | PSM_GHOST_SKIP_X, stream);
+      if (rc) return rc;
+      return history ? psm_residual(P, act.data(), steps, stream) : PSM_OK;
+    }
   }
   for (int s = 0; s < steps; ++s) {
     rc = psm_gs_sweep(P, act.data(), omega, gs_mode, stream);

@@ -56,6 +56,7 @@ struct PlaneFac {
   double fy_lo, fy_up;
   const double* Q;     // nx*nx orthonormal DST-I basis, symmetric
   const double* Qf;    // parity-split basis in DMMA fragment order (psm_plane_dst.cu)
+  int nconst;          // rows >= nconst of cp / invm equal row nconst bitwise (every mode)
   const double* cp;    // [mode][ny] Thomas factors
   const double* invm;  // [mode][ny]
   // banded factorised form (psm_plane_band.cu); bw == 0: not available
@@ -246,6 +247,8 @@ struct psm_plan {
   GsPipeState* gspipe = nullptr;
   int* d_gsflags = nullptr;  // nplanes progress words + one ticket per group
   int gs_ntickets = 0;
+  int* d_msflags = nullptr;   // multi-sweep line GS: steps * nplanes progress words + tickets
+  long long ms_flag_cap = 0;
   // physical ghosts the sweeps since the last refresh left to it: 0 none
   // (one-tile / generic line-Jacobi kernels: written in their epilogues), 1
   // the y/z faces (z-marching line Jacobi, plane and box Jacobi: x faces

@@ -39,6 +39,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "psm_internal.cuh"
@@ -61,7 +62,7 @@ struct GsUniform {
   int npcr;  // PCR steps until the remaining interface couplings are < 1e-20 (<= 5: exact)
 };
 
-template <int NC>
+template <int NC, int MS = 0>
 struct GCfg {
   static constexpr int IS = 32 + 16 / NC;      // stride between the NC "i-rows" of a slot
   static constexpr int SLOT = (NC * IS + 3) / 2 * 2;  // doubles per ring slot (+ the two x-ghosts), even: 16-B bulk copies
@@ -86,9 +87,14 @@ struct GCfg {
   // warp 0's ring: the lagged ghost plane u(j,-1) when k0 == 0 (cp.async,
   // chunk layout), else the new rows of plane k0-1 (TMA bulk, padded rows)
   static constexpr int MR = (D * SLOT > DM * MROW) ? D * SLOT : DM * MROW;
+  // multi-sweep mode (MS): the old rows travel beside the new ones (the
+  // history residual of the previous sweep needs u^{s-1}(j, k-1)): one old
+  // ring per warp hand-off, one for the publisher, one for warp 0's rows of
+  // plane k0-1 (from the boundary buffer)
+  static constexpr int OLD_DOUBLES = MS ? ((kGsW - 1) * DH * SLOT + DHL * SLOT + DM * MROW) : 0;
   static constexpr size_t SMEM =
-      (size_t)(HEAD_DOUBLES + (kGsW - 1) * WARP_DOUBLES + LAST_DOUBLES + MR) * sizeof(double);
-  static constexpr int MINB = NC >= 8 ? 1 : 2;
+      (size_t)(HEAD_DOUBLES + (kGsW - 1) * WARP_DOUBLES + LAST_DOUBLES + MR + OLD_DOUBLES) * sizeof(double);
+  static constexpr int MINB = (NC >= 8 || MS) ? 1 : 2;
   __device__ static __forceinline__ int pos(int x) { return (x % NC) * IS + x / NC; }
 };
 
@@ -178,13 +184,31 @@ __device__ long long g_gs_prof[16];
   } while (0)
 #endif
 
-template <int NC, int CHAOTIC, int UNIT>
-__global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
+// Multi-sweep mode (MS = 1; one patch whose faces are all physical): the
+// launch runs several GS steps, units (sweep s, k0) in s-major ticket order,
+// so sweep s+1 trails sweep s by a few wavefronts instead of waiting for it
+// to finish.  Every sweep has its own per-plane progress words (flags +
+// s * flag_stride: a single word per plane would let a later sweep's
+// progress stand in for an earlier one's); a unit of sweep s reads the old
+// rows u(j+1, k) and u(j, k+1) only
+// once sweep s-1 has published them (and, by the same wait, has consumed
+// the values it overwrites), so the arithmetic is exactly that of s
+// separate sweeps.  Ghost values are the step-end refresh's: every face is
+// physical, ghost = -(the adjacent interior cell's value after the previous
+// step), which each line has at hand as its own old value.  The history
+// residual of sweep s-1's result is formed while sweep s passes over each
+// cell (the old values of (j-1, k) and (j, k-1) travel beside the new ones;
+// a unit's first plane gets them from the boundary buffer `oldb`, written
+// by the previous unit's publisher) with the reference's operation order,
+// and summed per plane into hist slot s-1.
+template <int NC, int CHAOTIC, int UNIT, int MS>
+__global__ void __launch_bounds__(kGsThreads, GCfg<NC, MS>::MINB)
     line_gs_pipe_kernel(const PatchDev* __restrict__ patches, const unsigned char* __restrict__ active,
                         StencilDev st, double omega, int* __restrict__ flags, int* __restrict__ ticket,
                         const int2* __restrict__ units, int nunits, const double* __restrict__ lane_tab,
-                        const __grid_constant__ GsUniform T, int nl) {
-  using C = GCfg<NC>;
+                        const __grid_constant__ GsUniform T, int nl, double* __restrict__ hist,
+                        long long hist_stride, double* __restrict__ oldb, int flag_stride) {
+  using C = GCfg<NC, MS>;
   constexpr int M = NC - 1;  // locally eliminated cells per chunk
   const int nx = NC * nl;    // lanes nl..31 carry no cells (nx not 32*NC)
   constexpr int IS = C::IS, SLOT = C::SLOT, D = C::D, P = C::P, DH = C::DH, DHL = C::DHL, DM = C::DM;
@@ -207,6 +231,12 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
   double* HL = ring + (kGsW - 1) * C::WARP_DOUBLES + 3 * D * SLOT;  // last warp's new rows (DHL)
   const double* Hprev = Hr - C::WARP_DOUBLES;          // previous warp's new rows
   double* Mr = ring + (kGsW - 1) * C::WARP_DOUBLES + C::LAST_DOUBLES;
+  // MS: old-row rings (see GCfg::OLD_DOUBLES)
+  double* oldr = Mr + C::MR;
+  double* HO = oldr + (warp < kGsW - 1 ? warp : 0) * C::DH * SLOT;   // this warp's old rows -> next warp
+  const double* HOprev = oldr + (warp > 0 ? warp - 1 : 0) * C::DH * SLOT;
+  double* HLO = oldr + (kGsW - 1) * C::DH * SLOT;                     // last warp's old rows -> publisher
+  double* MrO = HLO + C::DHL * SLOT;                                  // warp 0: old rows of plane k0-1
   uint32_t mbase = 0;  // warp 0: TMA row loads completed in earlier units
 
   for (int e = threadIdx.x; e < kGsTab * 32; e += blockDim.x) tab[e] = lane_tab[e];
@@ -232,18 +262,24 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
     const int u = unit_sh[0];
     if (u >= nunits) return;
     const int2 U = units[u];
-    const PatchDev& Pd = patches[U.x];
+    const int sw = MS ? (U.x >> 16) : 0;   // sweep of this unit (MS)
+    const int pidx = MS ? (U.x & 0xffff) : U.x;
+    const PatchDev& Pd = patches[pidx];
     const int nz = Pd.nz, ny = Pd.ny;
     const long long px = nx + 2, pxy = px * (ny + 2);
-    double* Ub = Pd.buf[active[U.x]];
+    int* const fl = flags + (MS ? (long long)sw * flag_stride : 0);  // this sweep's progress words
+    double* Ub = Pd.buf[active[pidx]];
 
     if (warp == kGsW) {
       // ======================= publisher ====================================
       const int kl = U.y + kGsW - 1;  // plane of the last compute warp
       if (kl < nz) {
         double* row0 = Ub + (long long)(kl + 1) * pxy + px + 1;
-        int* my_flag = flags + Pd.plane0 + kl;
+        int* my_flag = fl + Pd.plane0 + kl;
         const bool succ = kl + 1 < nz;
+        // MS: the boundary buffer row of plane kl (old values, for the next
+        // unit's history residual)
+        double* ob = MS && succ ? oldb + (long long)(kl / kGsW) * ny * nx : nullptr;
         for (int j = 0; j < ny; ++j) {
           const int s = j % DHL;
           gs_mbar_wait(&fullL[s], (j / DHL) & 1);
@@ -252,11 +288,20 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
 #pragma unroll
           for (int i = 0; i < NC; ++i)
             if (i * 32 + lane < nx) __stcg(dst + i * 32 + lane, hs[dpos[i]]);
+          if (MS && ob) {
+            const double* ho = HLO + s * SLOT;
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+              if (i * 32 + lane < nx) __stcg(ob + (long long)j * nx + i * 32 + lane, ho[dpos[i]]);
+          }
           __syncwarp();
           if (lane == 0) {
             gs_mbar_arrive(&emptyL[s]);
-            if (succ) {
-              // release: cumulative over the warp's stores (warp barrier above)
+            // release: cumulative over the warp's stores (warp barrier above);
+            // MS: every sweep's rows are published (the next sweep waits on them)
+            if (MS) {
+              if ((j + 1) % kGsPub == 0 || j == ny - 1) st_release_gpu(my_flag, j + 1);
+            } else if (succ) {
               if (CHAOTIC) st_relaxed_gpu(my_flag, j + 1);
               else if ((j + 1) % kGsPub == 0 || j == ny - 1) st_release_gpu(my_flag, j + 1);
             }
@@ -270,9 +315,35 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
       const bool consumer = !last && (k + 1 < nz);
       double* row0 = Ub + (long long)(k + 1) * pxy + px + 1;  // u(0, 0, k)
       const double* Fk = Pd.f + (long long)k * ny * nx;
-      const int* dep_flag = flags + Pd.plane0 + k - 1;
+      const int* dep_flag = fl + Pd.plane0 + k - 1;
+      // MS, sweep >= 1: old rows of plane k (row j+1) and k+1 (row j) must be
+      // sweep sw-1's final values (lane 0 polls that sweep's words, caches
+      // what it saw)
+      const int* flag_k = fl - flag_stride + Pd.plane0 + k;
+      const int* flag_k1 = flag_k + 1;
+      int seen_k = 0, seen_k1 = 0;
+      auto await_old = [&](int j) {
+        if (!MS || sw == 0) return;
+        if (lane == 0) {
+          const int need_k = min(j + 2, ny), need_k1 = k + 1 < nz ? min(j + 1, ny) : 0;
+          if (seen_k < need_k || seen_k1 < need_k1) {
+            SpinGuard sg;
+            while (seen_k < need_k) {
+              seen_k = ld_relaxed_gpu(flag_k);
+              if (seen_k < need_k) sg.check();
+            }
+            while (seen_k1 < need_k1) {
+              seen_k1 = ld_relaxed_gpu(flag_k1);
+              if (seen_k1 < need_k1) sg.check();
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          }
+        }
+        __syncwarp();
+      };
 
       auto issue = [&](int j) {
+        if (j < ny) await_old(j);
         if (j < ny) {
           const int s = (j % D) * SLOT;
           const double* src_u = row0 + (long long)(j + 1) * px;
@@ -299,10 +370,15 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
       };
 
       double cen[NC], ym[NC];
+      double ymo[NC];   // MS: old u(j-1, k) (the previous row's cen before the update)
+      double hsum = 0.0;  // MS: sum of r^2 of sweep sw-1's result over this lane's cells of plane k
+      await_old(0);
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
         cen[i] = lane < nl ? row0[lane * NC + i] : 0.0;
-        ym[i] = lane < nl ? row0[lane * NC + i - px] : 0.0;
+        // MS: the ghost row j = -1 after the previous step's refresh is -u(0, k)
+        ym[i] = MS ? -cen[i] : (lane < nl ? row0[lane * NC + i - px] : 0.0);
+        ymo[i] = ym[i];
       }
 #pragma unroll
       for (int j = 0; j < P; ++j) issue(j);
@@ -318,14 +394,23 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
         __syncwarp();
         GS_PROF(1, 0.0);
         const int s = (j % D) * SLOT;
-        double nxt[NC], zp[NC], fv[NC], zm[NC];
+        double nxt[NC], zp[NC], fv[NC], zm[NC], zmo[NC];
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
           nxt[i] = Ur[s + i * IS + lane];
           zp[i] = Zr[s + i * IS + lane];
           fv[i] = Fr[s + i * IS + lane];
         }
-        const double gl = Ur[s + NC * IS], gr = Ur[s + NC * IS + 1];
+        double gl = Ur[s + NC * IS], gr = Ur[s + NC * IS + 1];
+        if (MS) {  // refreshed ghosts: -(own old end values), -(own old row / plane)
+          gl = -__shfl_sync(0xffffffffu, cen[0], 0);
+          gr = -__shfl_sync(0xffffffffu, cen[NC - 1], nl - 1);
+#pragma unroll
+          for (int i = 0; i < NC; ++i) {
+            if (j == ny - 1) nxt[i] = -cen[i];
+            if (k == nz - 1) zp[i] = -cen[i];
+          }
+        }
         GS_PROF(2, 0.0);
         // ---- residual prefix, reference order (stencil.py:106-111): c u,
         // -x, +x, -y, +y need nothing from plane k-1, so they run before the
@@ -360,11 +445,19 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           const double* h = Hprev + hs * SLOT;
 #pragma unroll
           for (int i = 0; i < NC; ++i) zm[i] = h[i * IS + lane];
+          if (MS) {
+            const double* ho = HOprev + hs * SLOT;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) zmo[i] = ho[i * IS + lane];
+          }
           __syncwarp();
           if (lane == 0) gs_mbar_arrive(&emptyH[(warp - 1) * DH + hs]);
         } else if (k == 0) {
 #pragma unroll
-          for (int i = 0; i < NC; ++i) zm[i] = Mr[s + i * IS + lane];
+          for (int i = 0; i < NC; ++i) {
+            zm[i] = MS ? -cen[i] : Mr[s + i * IS + lane];  // MS: refreshed ghost plane
+            zmo[i] = zm[i];
+          }
         } else {
           // new rows of plane k0-1 (previous CTA's publisher): TMA bulk copies
           // through L2 (never a stale L1 line), issued once published
@@ -372,15 +465,18 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
             if (avail <= j) {
               SpinGuard sg;
               while ((avail = ld_relaxed_gpu(dep_flag)) <= j) sg.check();
-              if (!CHAOTIC) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              if (!CHAOTIC || MS) asm volatile("fence.acq_rel.gpu;" ::: "memory");
               asm volatile("fence.proxy.async.global;" ::: "memory");
             }
             const int lim = min(avail, j + DM);
+            const double* ob = MS ? oldb + (long long)(k / kGsW - 1) * ny * nx : nullptr;
             for (; issued < lim; ++issued) {
               const uint32_t n = mbase + (uint32_t)issued;
-              gs_mbar_expect_tx(&mbarM[n % DM], (uint32_t)(px * 8));
+              gs_mbar_expect_tx(&mbarM[n % DM], (uint32_t)(px * 8) + (MS && sw > 0 ? (uint32_t)(nx * 8) : 0u));
               gs_tma_row(Mr + (n % DM) * MROW, row0 + (long long)issued * px - pxy - 1, (uint32_t)(px * 8),
                          &mbarM[n % DM]);
+              if (MS && sw > 0)
+                gs_tma_row(MrO + (n % DM) * MROW, ob + (long long)issued * nx, (uint32_t)(nx * 8), &mbarM[n % DM]);
             }
           }
           __syncwarp();
@@ -389,8 +485,44 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           const double* mrow = Mr + (n % DM) * MROW + 1 + lane * NC;
 #pragma unroll
           for (int i = 0; i < NC; ++i) zm[i] = mrow[i];
+          if (MS && sw > 0) {
+            const double* morow = MrO + (n % DM) * MROW + lane * NC;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) zmo[i] = morow[i];
+          }
         }
         GS_PROF(3, zm[NC - 1] + fv[NC - 1] + nxt[NC - 1] + zp[NC - 1]);
+        if (MS && sw > 0 && hist) {
+          // residual of sweep sw-1's result at this line (reference order:
+          // c u, -x, +x, -y, +y, -z, +z, then f - acc), all old values
+          const double lft = __shfl_up_sync(0xffffffffu, cen[NC - 1], 1);
+          const double rgt = __shfl_down_sync(0xffffffffu, cen[0], 1);
+#pragma unroll
+          for (int i = 0; i < NC; ++i) {
+            const double xl = i > 0 ? cen[i > 0 ? i - 1 : 0] : (lane == 0 ? gl : lft);
+            const double xr = i < NC - 1 ? cen[i < NC - 1 ? i + 1 : 0] : (lane == nl - 1 ? gr : rgt);
+            double a;
+            if (UNIT) {
+              a = __dmul_rn(st.c, cen[i]);
+              a = __dsub_rn(a, xl);
+              a = __dsub_rn(a, xr);
+              a = __dsub_rn(a, ymo[i]);
+              a = __dsub_rn(a, nxt[i]);
+              a = __dsub_rn(a, zmo[i]);
+              a = __dsub_rn(a, zp[i]);
+            } else {
+              a = __dmul_rn(st.c, cen[i]);
+              a = __dadd_rn(a, __dmul_rn(st.xm, xl));
+              a = __dadd_rn(a, __dmul_rn(st.xp, xr));
+              a = __dadd_rn(a, __dmul_rn(st.ym, ymo[i]));
+              a = __dadd_rn(a, __dmul_rn(st.yp, nxt[i]));
+              a = __dadd_rn(a, __dmul_rn(st.zm, zmo[i]));
+              a = __dadd_rn(a, __dmul_rn(st.zp, zp[i]));
+            }
+            const double rr = lane < nl ? __dsub_rn(fv[i], a) : 0.0;
+            hsum = fma(rr, rr, hsum);
+          }
+        }
         double r[NC];
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
@@ -447,6 +579,11 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           double* h = HL + hs * SLOT;
 #pragma unroll
           for (int i = 0; i < NC; ++i) h[i * IS + lane] = nv[i];
+          if (MS) {
+            double* ho = HLO + hs * SLOT;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) ho[i * IS + lane] = cen[i];
+          }
           __syncwarp();
           if (lane == 0) gs_mbar_arrive(&fullL[hs]);
         } else {
@@ -455,55 +592,83 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC>::MINB)
           double* h = Hr + hs * SLOT;
 #pragma unroll
           for (int i = 0; i < NC; ++i) h[i * IS + lane] = nv[i];
+          if (MS) {
+            double* ho = HO + hs * SLOT;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) ho[i * IS + lane] = cen[i];
+          }
           __syncwarp();
           if (consumer && lane == 0) gs_mbar_arrive(&fullH[warp * DH + hs]);
           double* dst = row0 + (long long)j * px;
 #pragma unroll
           for (int i = 0; i < NC; ++i)
             if (i * 32 + lane < nx) __stcg(dst + i * 32 + lane, h[dpos[i]]);
+          if (MS) {  // publish this plane's progress for the next sweep
+            __syncwarp();
+            if (lane == 0 && ((j + 1) % kGsPub == 0 || j == ny - 1)) st_release_gpu(fl + Pd.plane0 + k, j + 1);
+          }
         }
         issue(j + P);  // prefetch, off the hand-off critical path
         GS_PROF(8, 0.0);
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
           ym[i] = nv[i];
+          ymo[i] = cen[i];
           cen[i] = nxt[i];
         }
       }
       cp_wait<0>();
       if (warp == 0 && k > 0) mbase += (uint32_t)ny;
+      if (MS && sw > 0 && hist) {
+        // plane k's sum of sweep sw-1: fixed-order warp tree, into the first
+        // history tile of the plane (the plane's other tiles hold zero)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+        double* slot = hist + (long long)(sw - 1) * hist_stride + Pd.tile0 + (long long)k * Pd.tpp;
+        for (int t = lane; t < Pd.tpp; t += 32) slot[t] = t == 0 ? hsum : 0.0;
+      }
     }
     __syncthreads();
   }
 }
 
-template <int NC, int CH, int UN>
+template <int NC, int CH, int UN, int MS>
 static int gs_pipe_occ1() {
-  using C = GCfg<NC>;
-  cudaFuncSetAttribute(line_gs_pipe_kernel<NC, CH, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  using C = GCfg<NC, MS>;
+  cudaFuncSetAttribute(line_gs_pipe_kernel<NC, CH, UN, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, line_gs_pipe_kernel<NC, CH, UN>, kGsThreads, C::SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, line_gs_pipe_kernel<NC, CH, UN, MS>, kGsThreads, C::SMEM);
   return b;
 }
 template <int NC>
-static int gs_pipe_occupancy() {
-  return std::min(std::min(gs_pipe_occ1<NC, 0, 0>(), gs_pipe_occ1<NC, 0, 1>()),
-                  std::min(gs_pipe_occ1<NC, 1, 0>(), gs_pipe_occ1<NC, 1, 1>()));
+static int gs_pipe_occupancy(int ms = 0) {
+  if (ms)
+    return std::min(std::min(gs_pipe_occ1<NC, 0, 0, 1>(), gs_pipe_occ1<NC, 0, 1, 1>()),
+                    std::min(gs_pipe_occ1<NC, 1, 0, 1>(), gs_pipe_occ1<NC, 1, 1, 1>()));
+  return std::min(std::min(gs_pipe_occ1<NC, 0, 0, 0>(), gs_pipe_occ1<NC, 0, 1, 0>()),
+                  std::min(gs_pipe_occ1<NC, 1, 0, 0>(), gs_pipe_occ1<NC, 1, 1, 0>()));
 }
 
 template <int NC>
-static cudaError_t gs_pipe_launch(int chaotic, int unit, int grid, const PatchDev* patches,
+static cudaError_t gs_pipe_launch(int chaotic, int unit, int ms, int grid, const PatchDev* patches,
                                   const unsigned char* active, const StencilDev& st, double omega, int* flags,
                                   int* ticket, const int2* units, int nunits, const double* lane_tab,
-                                  const GsUniform& T, int nl, cudaStream_t s) {
-  using C = GCfg<NC>;
-#define PSM_GSP(CH, UN)                                                                                     \
-  line_gs_pipe_kernel<NC, CH, UN><<<grid, kGsThreads, C::SMEM, s>>>(patches, active, st, omega, flags, ticket, \
-                                                                    units, nunits, lane_tab, T, nl)
-  if (chaotic) {
-    if (unit) PSM_GSP(1, 1); else PSM_GSP(1, 0);
+                                  const GsUniform& T, int nl, double* hist, long long hist_stride, double* oldb,
+                                  int flag_stride, cudaStream_t s) {
+#define PSM_GSP(CH, UN, MS_)                                                                                 \
+  line_gs_pipe_kernel<NC, CH, UN, MS_><<<grid, kGsThreads, GCfg<NC, MS_>::SMEM, s>>>(                        \
+      patches, active, st, omega, flags, ticket, units, nunits, lane_tab, T, nl, hist, hist_stride, oldb, \
+      flag_stride)
+  if (ms) {
+    if (chaotic) {
+      if (unit) PSM_GSP(1, 1, 1); else PSM_GSP(1, 0, 1);
+    } else {
+      if (unit) PSM_GSP(0, 1, 1); else PSM_GSP(0, 0, 1);
+    }
+  } else if (chaotic) {
+    if (unit) PSM_GSP(1, 1, 0); else PSM_GSP(1, 0, 0);
   } else {
-    if (unit) PSM_GSP(0, 1); else PSM_GSP(0, 0);
+    if (unit) PSM_GSP(0, 1, 0); else PSM_GSP(0, 0, 0);
   }
 #undef PSM_GSP
   return cudaGetLastError();
@@ -530,6 +695,10 @@ struct GsPipeGroup {
 
 struct GsPipeState {
   std::vector<GsPipeGroup> groups;
+  // multi-sweep launches (one patch): units per step count, boundary buffer
+  std::map<int, std::pair<int2*, int>> ms_units;
+  double* oldb = nullptr;
+  int ms_occ = -1;
 };
 
 #ifdef PSM_GS_PROFILE
@@ -734,6 +903,8 @@ void psm_gs_pipe_free(psm_plan* P) {
     cudaFree(G.d_units);
     cudaFree(G.d_tab);
   }
+  for (auto& kv : P->gspipe->ms_units) cudaFree(kv.second.first);
+  cudaFree(P->gspipe->oldb);
   delete P->gspipe;
   P->gspipe = nullptr;
 }
@@ -758,9 +929,9 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
     int* tk = tickets + G.ticket;
     cudaStream_t s_main = s;
     if (fan) s = P->side[gi++ % psm_plan::kSide];
-#define PSM_GSL(N) \
-  gs_pipe_launch<N>(chaotic, unit, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits, G.d_tab, \
-                    G.T, G.nl, s)
+#define PSM_GSL(N)                                                                                                 \
+  gs_pipe_launch<N>(chaotic, unit, 0, G.grid, P->d_patches, da, P->st, omega, flags, tk, G.d_units, G.nunits,       \
+                    G.d_tab, G.T, G.nl, nullptr, 0, nullptr, 0, s)
     switch (G.nc) {
       case 1: e = PSM_GSL(1); break;
       case 2: e = PSM_GSL(2); break;
@@ -780,5 +951,81 @@ int psm_gs_pipe_sweep(psm_plan* P, const unsigned char* da, double omega, int ch
     const cudaError_t e = psm_side_join(P, s, ng);
     if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
   }
+  return PSM_OK;
+}
+
+// Several GS steps in one launch (multi-sweep mode of line_gs_pipe_kernel):
+// one patch, every face physical, a prepared pipeline with one group.
+// hist: history slots (slot s-1 gets the residual sums of step s's input,
+// s = 1..steps-1; null: none); flags: steps * nplanes progress words and
+// tickets, zeroed by the caller.
+bool psm_gs_pipe_multi_ok(const psm_plan* P) {
+  return P->gspipe && P->gspipe->groups.size() == 1 && P->npatch == 1 && P->ncopy == 0 &&
+         P->hp[0].iface == 0 && !P->hp[0].peer_lo[0] && !P->hp[0].peer_hi[0];
+}
+
+int psm_gs_pipe_multi(psm_plan* P, const unsigned char* da, double omega, int chaotic, int steps, double* hist,
+                      long long hist_stride, int* flags, int* tickets, cudaStream_t s) {
+  if (!psm_gs_pipe_multi_ok(P) || steps < 1 || steps >= 0x7fff)
+    return psm_set_error(PSM_EINVAL, "multi-sweep line GS needs one patch with physical faces");
+  GsPipeState* S = P->gspipe;
+  const GsPipeGroup& G = S->groups[0];
+  const PatchDev& h = P->hp[0];
+  auto it = S->ms_units.find(steps);
+  if (it == S->ms_units.end()) {
+    std::vector<int> uv;
+    for (int sw = 0; sw < steps; ++sw)
+      for (int k0 = 0; k0 < h.nz; k0 += kGsW) {
+        uv.push_back(sw << 16);
+        uv.push_back(k0);
+      }
+    int2* d = nullptr;
+    if (cudaMalloc(&d, uv.size() * sizeof(int)) != cudaSuccess)
+      return psm_set_error(PSM_ENOMEM, "cudaMalloc for multi-sweep GS units");
+    cudaMemcpy(d, uv.data(), uv.size() * sizeof(int), cudaMemcpyHostToDevice);
+    it = S->ms_units.emplace(steps, std::make_pair(d, (int)(uv.size() / 2))).first;
+  }
+  if (!S->oldb) {
+    const size_t n = (size_t)((h.nz + kGsW - 1) / kGsW) * h.ny * h.nx;
+    if (cudaMalloc(&S->oldb, n * sizeof(double)) != cudaSuccess)
+      return psm_set_error(PSM_ENOMEM, "cudaMalloc for the multi-sweep boundary rows");
+  }
+  if (S->ms_occ < 0) {
+    switch (G.nc) {
+      case 1: S->ms_occ = gs_pipe_occupancy<1>(1); break;
+      case 2: S->ms_occ = gs_pipe_occupancy<2>(1); break;
+      case 3: S->ms_occ = gs_pipe_occupancy<3>(1); break;
+      case 4: S->ms_occ = gs_pipe_occupancy<4>(1); break;
+      case 5: S->ms_occ = gs_pipe_occupancy<5>(1); break;
+      case 6: S->ms_occ = gs_pipe_occupancy<6>(1); break;
+      case 7: S->ms_occ = gs_pipe_occupancy<7>(1); break;
+      default: S->ms_occ = gs_pipe_occupancy<8>(1); break;
+    }
+  }
+  if (S->ms_occ < 1) return psm_set_error(PSM_ECUDA, "multi-sweep line GS kernel does not fit on an SM");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nunits = it->second.second;
+  const int grid = std::min(nunits, S->ms_occ * sms);
+  const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
+                    P->st.zm == -1.0 && P->st.zp == -1.0;
+  cudaError_t e;
+#define PSM_GSM(N)                                                                                             \
+  gs_pipe_launch<N>(chaotic, unit, 1, grid, P->d_patches, da, P->st, omega, flags, tickets + G.ticket,          \
+                    it->second.first, nunits, G.d_tab, G.T, G.nl, hist, hist_stride, S->oldb, P->nplanes, s)
+  switch (G.nc) {
+    case 1: e = PSM_GSM(1); break;
+    case 2: e = PSM_GSM(2); break;
+    case 3: e = PSM_GSM(3); break;
+    case 4: e = PSM_GSM(4); break;
+    case 5: e = PSM_GSM(5); break;
+    case 6: e = PSM_GSM(6); break;
+    case 7: e = PSM_GSM(7); break;
+    default: e = PSM_GSM(8); break;
+  }
+#undef PSM_GSM
+  if (e != cudaSuccess) return psm_set_error(PSM_ECUDA, cudaGetErrorString(e));
+  P->launches += 1;
   return PSM_OK;
 }

@@ -34,12 +34,11 @@ cudaError_t launch_plane_band_jacobi(int K, int BW, const PatchDev* patches, con
 void dst_split_table(const std::vector<double>& Q, int nx, std::vector<double>& out);
 size_t dst_table_doubles(int nx);
 int dst_max_nx();
-cudaError_t launch_dst_rows(int pro, int epi, const PatchDev* patches, int p0, int p1, long long c0, long long nrows,
-                            int nx, const double* qf, const unsigned char* active, const StencilDev& st,
-                            double omega, const double* in, double* out, cudaStream_t s);
-cudaError_t launch_plane_gs_chain(const PlaneFac* d_fac, int nx, const PatchDev* patches, int p0, int np, int maxnz,
-                                  double czw, double* buf, cudaStream_t s);
-enum { kDstProRows = 0, kDstProResidual = 1 };
+cudaError_t launch_dst_rows(int epi, const PatchDev* patches, int p0, int p1, long long c0, long long nrows, int nx,
+                            const double* qf, const unsigned char* active, double omega, const double* in,
+                            double* out, long long rows_per_patch, cudaStream_t s);
+cudaError_t launch_plane_gs_chain(const PlaneFac* d_fac, int nx, int ny, int nj, const PatchDev* patches, int p0,
+                                  int np, int maxnz, double czw, double* buf, cudaStream_t s);
 enum { kDstEpiStore = 0, kDstEpiRelaxInPlace = 1, kDstEpiRelaxInto = 2 };
 cudaError_t launch_line_tiles(int mode, const PatchDev* patches, int npatch, const unsigned char* active,
                               const StencilDev& st, double omega, double* partials, double* rbuf, long long tile_base,
@@ -339,6 +338,18 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
   H.nj = nj;
   H.H = band.empty() ? nullptr : tab + nq + 2 * nt;
   H.Qf = qf.empty() ? nullptr : tab + nq + 2 * nt + band.size();
+  // first row from which both Thomas tables stay bitwise constant
+  H.nconst = 0;
+  for (int j = ny - 1; j > 0; --j) {
+    bool same = true;
+    for (int i = 0; i < nx && same; ++i)
+      same = invm[(size_t)j * nx + i] == invm[(size_t)(j - 1) * nx + i] &&
+             cp[(size_t)j * nx + i] == cp[(size_t)(j - 1) * nx + i];
+    if (!same) {
+      H.nconst = j;
+      break;
+    }
+  }
   F->d_plane = (PlaneFac*)F->dev;
   PCUDA(cudaMemcpy(F->dev, &H, sizeof H, cudaMemcpyHostToDevice));
   PCUDA(cudaMemcpy(tab, Q.data(), nq * sizeof(double), cudaMemcpyHostToDevice));
@@ -357,9 +368,7 @@ int psm_plane_build(const psm_stencil* st, int nx, int ny, psm_factors* F) {
 static int dst_rows(const PlaneFac& h, const double* in, double* out, long long nvec, cudaStream_t s) {
   if (!h.Qf)
     return psm_set_error(PSM_EUNSUPPORTED, "DST plane transforms support nx <= 512 (use the banded plane solver)");
-  static const StencilDev none{};
-  PCUDA(launch_dst_rows(kDstProRows, kDstEpiStore, nullptr, 0, 0, 0, nvec, h.nx, h.Qf, nullptr, none, 0.0, in, out,
-                        s));
+  PCUDA(launch_dst_rows(kDstEpiStore, nullptr, 0, 0, 0, nvec, h.nx, h.Qf, nullptr, 0.0, in, out, 0, s));
   return PSM_OK;
 }
 
@@ -448,6 +457,13 @@ int psm_plane_plan_free(psm_plan* P) {
   return PSM_OK;
 }
 
+// rows of each patch of a run when they are all equal (ny * nz), else 0
+static long long run_rows_per_patch(const psm_plan* P, const PlaneRun& r) {
+  for (int p = r.p0 + 1; p < r.p1; ++p)
+    if (P->hp[p].nz != P->hp[r.p0].nz) return 0;
+  return (long long)P->hp[r.p0].ny * P->hp[r.p0].nz;
+}
+
 // Jacobi: residual of every cell (tile kernel, mode 2 stores r and the
 // history partials), then per run of patches sharing a factor either the
 // banded factorised solve (writes v directly) or DST -> modal Thomas -> DST
@@ -486,8 +502,8 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
     if (rc) return rc;
     launch_modal_thomas(*r.h_fac, r.d_fac, S->rhat + c0, planes, s);
     PCUDA(cudaGetLastError());
-    PCUDA(launch_dst_rows(kDstProRows, kDstEpiRelaxInto, P->d_patches, r.p0, r.p1, c0, nvec, r.nx, r.Qf, da, P->st,
-                          omega, S->rhat + c0, nullptr, s));
+    PCUDA(launch_dst_rows(kDstEpiRelaxInto, P->d_patches, r.p0, r.p1, c0, nvec, r.nx, r.Qf, da, omega, S->rhat + c0,
+                          nullptr, run_rows_per_patch(P, r), s));
     P->launches += 3;
   }
   if (fan) PCUDA(psm_side_join(P, s, nband));
@@ -509,6 +525,11 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
   for (const PlaneRun& r : S->runs)
     if (!r.Qf) return psm_set_error(PSM_EUNSUPPORTED, "plane GS supports nx <= 512");
   const double czw = P->st.zm * omega;
+  // 1. the pre-sweep residual of every cell (z-marching line kernel, r only)
+  {
+    const int rc = psm_plane_residual(P, da, P->d_scratch, S->rbuf, s);
+    if (rc) return rc;
+  }
   for (const PlaneRun& r : S->runs) {
     const long long c0 = P->hp[r.p0].cell0;
     long long planes = 0;
@@ -517,14 +538,18 @@ int psm_plane_gs(psm_plan* P, const unsigned char* da, double omega, cudaStream_
       planes += P->hp[p].nz;
       maxnz = std::max(maxnz, P->hp[p].nz);
     }
-    // 1. rhat = Q r_pre: the pre-sweep residual of every row, transformed
-    PCUDA(launch_dst_rows(kDstProResidual, kDstEpiStore, P->d_patches, r.p0, r.p1, c0, planes * r.ny, r.nx, r.Qf, da,
-                          P->st, 0.0, nullptr, S->rhat + c0, s));
+    // rhat = Q r_pre
+    {
+      const int rc = dst_rows(*r.h_fac, S->rbuf + c0, S->rhat + c0, planes * r.ny, s);
+      if (rc) return rc;
+    }
     // 2. every (patch, mode) chain over the stages k, one launch
-    PCUDA(launch_plane_gs_chain(r.d_fac, r.nx, P->d_patches, r.p0, r.p1 - r.p0, maxnz, czw, S->rhat + c0, s));
+    // (the chain kernel addresses planes by the patches' global cell0)
+    PCUDA(launch_plane_gs_chain(r.d_fac, r.nx, r.ny, r.h_fac->nconst, P->d_patches, r.p0, r.p1 - r.p0, maxnz, czw,
+                                S->rhat, s));
     // 3. x = Q xhat, relaxed into u in place
-    PCUDA(launch_dst_rows(kDstProRows, kDstEpiRelaxInPlace, P->d_patches, r.p0, r.p1, c0, planes * r.ny, r.nx, r.Qf,
-                          da, P->st, omega, S->rhat + c0, nullptr, s));
+    PCUDA(launch_dst_rows(kDstEpiRelaxInPlace, P->d_patches, r.p0, r.p1, c0, planes * r.ny, r.nx, r.Qf, da, omega,
+                          S->rhat + c0, nullptr, run_rows_per_patch(P, r), s));
     P->launches += 3;
   }
   return PSM_OK;

@@ -29,9 +29,12 @@
 #include <math.h>
 
 #include <algorithm>
+#include <stdlib.h>
+
 #include <atomic>
 #include <vector>
 
+#include "psm_async.cuh"
 #include "psm_internal.cuh"
 
 namespace psm {
@@ -79,139 +82,209 @@ struct DstRun {
   const double* qf;  // split table, fragment order [parity][ks][nt][lane]
 };
 
-enum { kProRows = 0, kProResidual = 1 };
+enum { kProRows = 0 };
 enum { kEpiStore = 0, kEpiRelaxInPlace = 1, kEpiRelaxInto = 2 };
 
-template <int KSM, int PRO, int EPI, bool QSM>
-__global__ void __launch_bounds__(kDstThreads) dst_tile_kernel(const DstRun R, const unsigned char* __restrict__ active,
-                                                               const StencilDev st, double omega,
-                                                               const double* __restrict__ in, double* __restrict__ out) {
+// shared-memory layout of one launch
+struct DstSmem {
+  int ldu;          // u-row stride (EPI relax): [x = -1 .. nx], even
+  int nstage;       // 1 or 2 (double-buffered input)
+  size_t q, stage, ustage;  // doubles
+  __host__ __device__ size_t total(bool relax) const {
+    return q + nstage * (stage + (relax ? ustage : 0));
+  }
+};
+// relax: stage the u rows too (EPI relax; else the epilogue reads u directly)
+__host__ __device__ inline DstSmem dst_smem(int nx, bool qsm, bool relax, int nstage) {
+  const DstGeom G = dst_geom(nx);
+  DstSmem m;
+  m.ldu = (nx + 2 + 1) / 2 * 2;
+  m.nstage = nstage;
+  m.q = qsm ? G.qdoubles : 0;
+  m.stage = (size_t)kDstRows * G.ld;
+  m.ustage = relax ? (size_t)kDstRows * m.ldu : 0;
+  return m;
+}
+
+// Warp-specialised pipeline: warp 8 produces, warps 0-7 consume.  The
+// producer maps each tile row to its patch, plane and row and streams the
+// rows in with the TMA engine (one bulk copy per row into a padded shared
+// row; with EPI relax also the row's u values, ghosts included) into a ring
+// of NST stages, throttled by the consumers' "empty" arrivals; rows that are
+// not 16-byte aligned (odd nx or odd workspace offset) it loads itself.  The
+// consumers run split-DST MMA and epilogue per tile, synchronising among
+// themselves only (named barrier 1), so loads for later tiles overlap them.
+constexpr int kDstConsumers = 256;
+constexpr int kDstAllThreads = kDstConsumers + 32;
+constexpr int kDstStages = 3;
+
+template <int KSM, int EPI, bool QSM, bool BULK>
+__global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRun R, const unsigned char* __restrict__ active,
+                                                                     double omega, const double* __restrict__ in,
+                                                                     double* __restrict__ out, int nstage, int ustaged,
+                                                                     long long rows_per_patch) {
+  constexpr bool RELAX = EPI != kEpiStore;
   extern __shared__ __align__(16) double dsm[];
   const int nx = R.nx;
   const DstGeom G = dst_geom(nx);
+  const DstSmem M = dst_smem(nx, QSM, RELAX && ustaged, nstage);
   double* qs = dsm;
-  double* tile = dsm + (QSM ? G.qdoubles : 0);
-  __shared__ int row_patch[kDstRows], row_k[kDstRows], row_j[kDstRows];
+  double* stage0 = dsm + M.q;
+  __shared__ uint64_t full[kDstStages], empty[kDstStages];
+  __shared__ int row_patch[kDstStages][kDstRows];
+  __shared__ long long row_base[kDstStages][kDstRows];  // u index of (x = 0, j, k) in the row's patch buffer
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int mt = warp & 3, par = warp >> 2;
-  if (QSM)
-    for (size_t e = tid; e < G.qdoubles; e += kDstThreads) qs[e] = __ldg(R.qf + e);
   const long long ntiles = (R.nrows + kDstRows - 1) / kDstRows;
   const int half = nx >> 1, mid = (nx & 1) ? half : -1;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long g0 = t * kDstRows;
-    if (tid < kDstRows) {
-      const long long g = g0 + tid;
-      int p = -1, k = 0, j = 0;
-      if (g < R.nrows && (PRO == kProResidual || EPI != kEpiStore)) {
-        const long long cell = R.c0 + g * nx;
-        int lo = R.p0, hi = R.p1 - 1;
-        while (lo < hi) {
-          const int m = (lo + hi + 1) >> 1;
-          if (R.patches[m].cell0 <= cell) lo = m; else hi = m - 1;
+  auto stage = [&](int s) { return stage0 + (size_t)s * (M.stage + M.ustage); };
+  auto ustage = [&](int s) { return stage0 + (size_t)s * (M.stage + M.ustage) + M.stage; };
+
+  if (tid == 0) {
+    for (int i = 0; i < kDstStages; ++i) {
+      async::bar_init(&full[i], 1);
+      async::bar_init(&empty[i], 1);
+    }
+    async::bar_fence_init();
+  }
+  if (QSM)
+    for (size_t e = tid; e < G.qdoubles; e += kDstAllThreads) qs[e] = __ldg(R.qf + e);
+  __syncthreads();
+
+  if (warp == kDstConsumers / 32) {
+    // ============================ producer ==================================
+    int it = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int s = it % nstage;
+      if (it >= nstage) async::bar_wait(&empty[s], ((it / nstage) - 1) & 1);
+      const long long g = t * kDstRows + lane;
+      const bool valid = g < R.nrows;
+      const int nvalid = (int)min((long long)kDstRows, R.nrows - t * kDstRows);
+      int p = 0;
+      long long ub = 0;
+      if (RELAX && valid) {
+        if (rows_per_patch > 0) {
+          p = R.p0 + (int)(g / rows_per_patch);
+        } else {
+          const long long cell = R.c0 + g * nx;
+          int lo = R.p0, hi = R.p1 - 1;
+          while (lo < hi) {
+            const int m = (lo + hi + 1) >> 1;
+            if (R.patches[m].cell0 <= cell) lo = m; else hi = m - 1;
+          }
+          p = lo;
         }
-        p = lo;
-        const long long e = (cell - R.patches[p].cell0) / nx;
-        const int ny = R.patches[p].ny;
-        k = (int)(e / ny);
-        j = (int)(e - (long long)k * ny);
+        const PatchDev& P = R.patches[p];
+        const long long e = (R.c0 + g * nx - P.cell0) / nx;
+        const int k = (int)(e / P.ny), j = (int)(e - (long long)k * P.ny);
+        ub = (long long)(k + 1) * (nx + 2) * (P.ny + 2) + (long long)(j + 1) * (nx + 2) + 1;
+        row_patch[s][lane] = p;
+        row_base[s][lane] = ub;
       }
-      row_patch[tid] = p;
-      row_k[tid] = k;
-      row_j[tid] = j;
-    }
-    __syncthreads();  // row map ready; the previous tile's epilogue is done with the tile
-    // ---- prologue: the tile's rows -------------------------------------
-    for (int r = warp; r < kDstRows; r += kDstThreads / 32) {
-      double* trow = tile + r * G.ld;
-      const long long g = g0 + r;
-      if (g >= R.nrows) {
-        for (int x = lane; x < nx; x += 32) trow[x] = 0.0;
-        continue;
-      }
-      if (PRO == kProRows) {
-        const double* src = in + g * nx;
-        for (int x = lane; x < nx; x += 32) trow[x] = src[x];
+      const bool us = RELAX && ustaged;
+      if (BULK) {
+        if (lane == 0)
+          async::bar_expect(&full[s], (uint32_t)nvalid * ((uint32_t)nx * 8u + (us ? (uint32_t)(nx + 2) * 8u : 0u)));
+        __syncwarp();
+        if (valid) {
+          async::bulk_g2s(stage(s) + lane * G.ld, in + g * nx, (uint32_t)nx * 8u, &full[s]);
+          if (us) {
+            const double* u = R.patches[p].buf[active[p]] + ub - 1;  // x = -1: even offset, 16-B aligned
+            async::bulk_g2s(ustage(s) + lane * M.ldu, u, (uint32_t)(nx + 2) * 8u, &full[s]);
+          }
+        }
       } else {
-        const PatchDev& P = R.patches[row_patch[r]];
-        const int k = row_k[r], j = row_j[r];
-        const long long px = nx + 2, pxy = px * (P.ny + 2);
-        const double* u = P.buf[active[row_patch[r]]] + (k + 1) * pxy + (j + 1) * px + 1;
-        const double* f = P.f + ((long long)k * P.ny + j) * nx;
-        for (int x = lane; x < nx; x += 32)
-          trow[x] = residual7(st, f[x], u[x], u[x - 1], u[x + 1], u[x - px], u[x + px], u[x - pxy], u[x + pxy]);
+        __syncwarp();
+        for (int r = 0; r < nvalid; ++r) {
+          const double* src = in + (t * kDstRows + r) * nx;
+          for (int x = lane; x < nx; x += 32) stage(s)[r * G.ld + x] = src[x];
+          if (us) {
+            const int pr = row_patch[s][r];
+            const double* u = R.patches[pr].buf[active[pr]] + row_base[s][r] - 1;
+            for (int x = lane; x < nx + 2; x += 32) ustage(s)[r * M.ldu + x] = u[x];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) async::bar_arrive(&full[s]);
       }
     }
-    __syncthreads();
+    return;
+  }
+
+  // ============================== consumers ===================================
+  const int mt = warp & 3, par = warp >> 2;
+  int it = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % nstage;
+    async::bar_wait(&full[s], (it / nstage) & 1);
+    double* st = stage(s);
+    const int nvalid = (int)min((long long)kDstRows, R.nrows - t * kDstRows);
     // ---- split DST: this warp's 8 rows x one parity ----------------------
-    // A fragments (pair sums / differences) for the whole K go to registers,
-    // then a barrier: after it no warp reads the tile, so the outputs
-    // overwrite it in place
-    const double* arow = tile + (8 * mt + (lane >> 2)) * G.ld;
+    // A fragments (pair sums / differences) for the whole K go to registers;
+    // after the barrier no warp reads the rows, so outputs overwrite them
+    const int arow_i = 8 * mt + (lane >> 2);
+    const double* arow = st + arow_i * G.ld;
+    const bool arow_ok = arow_i < nvalid;
     const double sgn = par ? -1.0 : 1.0;
     double a[KSM];
 #pragma unroll
-    for (int s = 0; s < KSM; ++s) {
-      const int p = 4 * s + (lane & 3);
+    for (int q = 0; q < KSM; ++q) {
+      const int p = 4 * q + (lane & 3);
       double v = 0.0;
-      if (p < half) v = arow[p] + sgn * arow[nx - 1 - p];
-      else if (p == mid && par == 0) v = arow[p];
-      a[s] = v;
+      if (arow_ok) {
+        if (p < half) v = arow[p] + sgn * arow[nx - 1 - p];
+        else if (p == mid && par == 0) v = arow[p];
+      }
+      a[q] = v;
     }
-    __syncthreads();
+    async::named_sync(1, kDstConsumers);
     {
       const double* qb = (QSM ? qs : R.qf) + (size_t)par * G.ks * G.nt * 32 + lane;
-      // output (row, m = 8 nt + 2 (lane&3) + c) of parity par is x index
-      // 2m + par, stored de-interleaved at column par * odd_off + m
-      double* orow = tile + (8 * mt + (lane >> 2)) * G.ld + par * G.odd_off;
+      // output (row, m = 8 nt + 2 (lane&3) + c) of parity par is x = 2 m + par
+      double* orow = st + arow_i * G.ld + par;
       const int cnt = par ? half : nx - half;  // outputs of this parity
       for (int n0 = 0; n0 < G.nt; n0 += kDstNG) {
         double acc[kDstNG][2];
 #pragma unroll
         for (int q = 0; q < kDstNG; ++q) acc[q][0] = acc[q][1] = 0.0;
 #pragma unroll
-        for (int s = 0; s < KSM; ++s) {
-          if (s < G.ks) {
+        for (int ks = 0; ks < KSM; ++ks) {
+          if (ks < G.ks) {
 #pragma unroll
             for (int q = 0; q < kDstNG; ++q) {
-              const size_t o = ((size_t)s * G.nt + n0 + q) * 32;
+              const size_t o = ((size_t)ks * G.nt + n0 + q) * 32;
               const double b = QSM ? qb[o] : __ldg(qb + o);
-              dmma884(acc[q][0], acc[q][1], a[s], b);
+              dmma884(acc[q][0], acc[q][1], a[ks], b);
             }
           }
         }
 #pragma unroll
         for (int q = 0; q < kDstNG; ++q) {
           const int m = 8 * (n0 + q) + 2 * (lane & 3);
-          if (m < cnt) orow[m] = acc[q][0];
-          if (m + 1 < cnt) orow[m + 1] = acc[q][1];
+          if (m < cnt) orow[2 * m] = acc[q][0];
+          if (m + 1 < cnt) orow[2 * m + 2] = acc[q][1];
         }
       }
     }
-    __syncthreads();
-    // ---- epilogue: rows back, x order ------------------------------------
-    for (int r = warp; r < kDstRows; r += kDstThreads / 32) {
-      const long long g = g0 + r;
-      if (g >= R.nrows) continue;
-      const double* trow = tile + r * G.ld;
+    async::named_sync(1, kDstConsumers);
+    // ---- epilogue: coalesced row stores ---------------------------------
+    for (int r = warp; r < nvalid; r += kDstConsumers / 32) {
+      const double* trow = st + r * G.ld;
+      const long long g = t * kDstRows + r;
       if (EPI == kEpiStore) {
         double* dst = out + g * nx;
-        for (int x = lane; x < nx; x += 32) dst[x] = trow[(x & 1) * G.odd_off + (x >> 1)];
+        for (int x = lane; x < nx; x += 32) dst[x] = trow[x];
       } else {
-        const int p = row_patch[r];
+        const int p = row_patch[s][r];
         const PatchDev& P = R.patches[p];
-        const int k = row_k[r], j = row_j[r];
-        const long long px = nx + 2, pxy = px * (P.ny + 2);
-        const long long base = (k + 1) * pxy + (j + 1) * px + 1;
         const int act = active[p];
+        const double* uo = ustaged ? ustage(s) + r * M.ldu + 1 : P.buf[act] + row_base[s][r];  // x = 0
         if (EPI == kEpiRelaxInPlace) {
-          double* u = P.buf[act] + base;
-          for (int x = lane; x < nx; x += 32) u[x] = relax(u[x], omega, trow[(x & 1) * G.odd_off + (x >> 1)]);
+          double* u = P.buf[act] + row_base[s][r];
+          for (int x = lane; x < nx; x += 32) u[x] = relax(uo[x], omega, trow[x]);
         } else {
-          const double* u = P.buf[act] + base;
-          double* v = P.buf[act ^ 1] + base;
+          double* v = P.buf[act ^ 1] + row_base[s][r];
           for (int x = lane; x < nx; x += 32) {
-            const double nv = relax(u[x], omega, trow[(x & 1) * G.odd_off + (x >> 1)]);
+            const double nv = relax(uo[x], omega, trow[x]);
             v[x] = nv;
             if (x == 0) v[-1] = -nv;
             if (x == nx - 1) v[nx] = -nv;
@@ -219,6 +292,8 @@ __global__ void __launch_bounds__(kDstThreads) dst_tile_kernel(const DstRun R, c
         }
       }
     }
+    async::named_sync(1, kDstConsumers);  // every consumer is done with stage s
+    if (tid == 0) async::bar_arrive(&empty[s]);
   }
 }
 
@@ -313,6 +388,90 @@ __global__ void __launch_bounds__(128) plane_gs_chain_kernel(const PlaneFac* __r
   }
 }
 
+// The same chains, each thread keeping its half-line's xhat(k-1) on chip
+// across the stages (a private shared-memory column: conflict-free [jj][tid]
+// layout) while plane k+1's transformed residuals stream into shared memory
+// (cp.async, double-buffered) during plane k's solve; the Thomas factors
+// come from shared memory too (rows jj < nj, then the converged row nj: the
+// tables are bitwise constant from there on, checked on the host).  Global
+// traffic is one read and one write of every value.  One CTA = 64 modes of
+// one patch, two threads per mode.
+__global__ void __launch_bounds__(128, 1) plane_gs_chain_smem_kernel(const PlaneFac* __restrict__ F,
+                                                                     const PatchDev* __restrict__ patches, int p0,
+                                                                     int cpp, int maxnz, double czw,
+                                                                     double* __restrict__ buf, int nj) {
+  extern __shared__ __align__(16) double csm[];
+  const int nx = F->nx, ny = F->ny, m = ny / 2, hmax = ny - m;
+  const int tid = threadIdx.x, q = tid >> 1, bot = tid & 1;
+  const int pl = blockIdx.x / cpp, i0 = (blockIdx.x - pl * cpp) * 64;
+  const int i = i0 + q;
+  const bool valid = i < nx;
+  const PatchDev& P = patches[p0 + pl];
+  const int nz = P.nz;
+  double* stg = csm;                              // [2][ny][64] transformed residuals
+  double* X = stg + 2 * (size_t)ny * 64 + tid;    // [hmax][128] this thread's column
+  double* fin = csm + 2 * (size_t)ny * 64 + (size_t)hmax * 128;  // [nj+1][64] 1/m
+  double* fcp = fin + (size_t)(nj + 1) * 64;                      // [nj+1][64] c'
+  for (int e = tid; e < (nj + 1) * 64; e += 128) {
+    const int jj = e >> 6, ii = i0 + (e & 63);
+    const long long o = (long long)jj * nx + ii;
+    fin[e] = ii < nx ? F->invm[o] : 1.0;
+    fcp[e] = ii < nx ? F->cp[o] : 0.0;
+  }
+  const double lo = F->fy_lo;
+  const int len = bot ? ny - m : m;
+  const long long plane_cells = (long long)nx * ny;
+  // this thread's rows: jj -> row0 + jj * drow
+  const int row0 = bot ? ny - 1 : 0, drow = bot ? -1 : 1;
+  auto load = [&](int k, int sidx) {
+    if (valid && k < nz) {
+      const double* src = buf + P.cell0 + (long long)k * plane_cells + i + (long long)row0 * nx;
+      double* dst = stg + (size_t)sidx * ny * 64 + q + row0 * 64;
+      for (int jj = 0; jj < len; ++jj) async::cp8(dst + jj * drow * 64, src + (long long)jj * drow * nx);
+    }
+    async::cp_commit();
+  };
+  __syncthreads();
+  for (int jj = 0; jj < len; ++jj) X[jj * 128] = 0.0;
+  const double* finq = fin + q;
+  const double* fcpq = fcp + q;
+  const double c_own = len > 0 ? fcpq[min(len - 1, nj) * 64] : 0.0;
+  load(0, 0);
+  for (int k = 0; k < maxnz; ++k) {
+    load(k + 1, (k + 1) & 1);
+    async::cp_wait<1>();  // plane k (this thread's own copies) landed
+    const double* S = stg + (size_t)(k & 1) * ny * 64 + q + row0 * 64;
+    const bool act = valid && k < nz;
+    double prev = 0.0;
+    if (act) {
+#pragma unroll 8
+      for (int jj = 0; jj < len; ++jj) {
+        double v = S[jj * drow * 64];
+        if (k > 0) v = fma(-czw, X[jj * 128], v);
+        prev = fma(-lo, prev, v) * finq[min(jj, nj) * 64];
+        X[jj * 128] = prev;
+      }
+    }
+    const double y_oth = __shfl_xor_sync(0xffffffffu, prev, 1);
+    const double c_oth = __shfl_xor_sync(0xffffffffu, c_own, 1);
+    if (act && len > 0) {
+      const double yT = bot ? y_oth : prev, yB = bot ? prev : y_oth;
+      const double cT = bot ? c_oth : c_own, cB = bot ? c_own : c_oth;
+      const double xT = (yT - cT * yB) / (1.0 - cT * cB);
+      double next = bot ? yB - cB * xT : xT;
+      double* dst = buf + P.cell0 + (long long)k * plane_cells + i + (long long)row0 * nx;
+      X[(len - 1) * 128] = next;
+      dst[(long long)(len - 1) * drow * nx] = next;
+#pragma unroll 8
+      for (int jj = len - 2; jj >= 0; --jj) {
+        next = fma(-fcpq[min(jj, nj) * 64], next, X[jj * 128]);
+        X[jj * 128] = next;
+        dst[(long long)jj * drow * nx] = next;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 int dst_max_nx() { return 512; }
 
@@ -337,12 +496,13 @@ void dst_split_table(const std::vector<double>& Q, int nx, std::vector<double>& 
 
 size_t dst_table_doubles(int nx) { return dst_geom(nx).qdoubles; }
 
-template <int KSM, int PRO, int EPI, bool QSM>
-static cudaError_t dst_launch_t(const DstRun& R, const unsigned char* active, const StencilDev& st, double omega,
-                                const double* in, double* out, cudaStream_t s) {
-  const DstGeom G = dst_geom(R.nx);
-  const size_t smem = ((QSM ? G.qdoubles : 0) + (size_t)kDstRows * G.ld) * sizeof(double);
-  auto kern = dst_tile_kernel<KSM, PRO, EPI, QSM>;
+template <int KSM, int EPI, bool QSM, bool BULK>
+static cudaError_t dst_launch_t(const DstRun& R, const unsigned char* active, double omega, const double* in,
+                                double* out, int nstage, int ustaged, long long rpp, cudaStream_t s) {
+  const bool us = EPI != kEpiStore && ustaged;
+  const DstSmem M = dst_smem(R.nx, QSM, us, nstage);
+  const size_t smem = M.total(us) * sizeof(double);
+  auto kern = dst_tile_kernel<KSM, EPI, QSM, BULK>;
   // the opt-in is per device and this size depends on nx: set it per launch
   // (host-side, no stream work)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -350,50 +510,83 @@ static cudaError_t dst_launch_t(const DstRun& R, const unsigned char* active, co
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDstThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDstAllThreads, smem);
   const long long ntiles = (R.nrows + kDstRows - 1) / kDstRows;
   const long long grid = std::max<long long>(1, std::min<long long>(ntiles, (long long)std::max(occ, 1) * sms));
-  kern<<<(unsigned)grid, kDstThreads, smem, s>>>(R, active, st, omega, in, out);
+  kern<<<(unsigned)grid, kDstAllThreads, smem, s>>>(R, active, omega, in, out, nstage, ustaged, rpp);
   return cudaGetLastError();
 }
 
-template <int PRO, int EPI>
-static cudaError_t dst_launch_k(const DstRun& R, const unsigned char* active, const StencilDev& st, double omega,
-                                const double* in, double* out, cudaStream_t s) {
+template <int EPI>
+static cudaError_t dst_launch_k(const DstRun& R, const unsigned char* active, double omega, const double* in,
+                                double* out, long long rpp, cudaStream_t s) {
   const DstGeom G = dst_geom(R.nx);
-  // the split table in shared memory when two CTAs per SM still fit
-  const bool qsm = (G.qdoubles + (size_t)kDstRows * G.ld) * sizeof(double) <= 112 * 1024;
-#define PSM_DST(K_)                                                                        \
-  return qsm ? dst_launch_t<K_, PRO, EPI, true>(R, active, st, omega, in, out, s)           \
-             : dst_launch_t<K_, PRO, EPI, false>(R, active, st, omega, in, out, s)
-  if (G.ks <= 8) PSM_DST(8);
-  if (G.ks <= 16) PSM_DST(16);
-  if (G.ks <= 32) PSM_DST(32);
+  constexpr bool relax = EPI != kEpiStore;
+  const size_t cap = 227 * 1024 - 2048;  // opt-in limit less the static shared memory
+  // preference: split table on chip, three then two input stages, staged u
+  // rows; dropped in the reverse order until the layout fits
+  bool qsm = true;
+  int nstage = kDstStages, ustaged = relax ? 1 : 0;
+  auto fits = [&] { return dst_smem(R.nx, qsm, ustaged, nstage).total(ustaged) * 8 <= cap; };
+  if (!fits()) nstage = 2;
+  if (!fits()) qsm = false;
+  if (!fits()) nstage = kDstStages;
+  if (!fits()) nstage = 2;
+  if (!fits()) ustaged = 0;
+  if (!fits()) nstage = 1;
+  if (!fits()) return cudaErrorInvalidValue;
+  // bulk copies need 16-byte aligned rows: even nx and an even workspace offset
+  const bool bulk = (R.nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
+#define PSM_DST(K_)                                                                                   \
+  if (qsm)                                                                                            \
+    return bulk ? dst_launch_t<K_, EPI, true, true>(R, active, omega, in, out, nstage, ustaged, rpp, s)     \
+                : dst_launch_t<K_, EPI, true, false>(R, active, omega, in, out, nstage, ustaged, rpp, s);   \
+  return bulk ? dst_launch_t<K_, EPI, false, true>(R, active, omega, in, out, nstage, ustaged, rpp, s)      \
+              : dst_launch_t<K_, EPI, false, false>(R, active, omega, in, out, nstage, ustaged, rpp, s)
+  if (G.ks <= 8) { PSM_DST(8); }
+  if (G.ks <= 16) { PSM_DST(16); }
+  if (G.ks <= 32) { PSM_DST(32); }
   PSM_DST(64);
 #undef PSM_DST
 }
 
-// rows -> transformed rows (or fused residual / relax, see the enums)
-cudaError_t launch_dst_rows(int pro, int epi, const PatchDev* patches, int p0, int p1, long long c0, long long nrows,
-                            int nx, const double* qf, const unsigned char* active, const StencilDev& st,
-                            double omega, const double* in, double* out, cudaStream_t s) {
+// rows -> transformed rows (EPI store), or relaxed into the patches
+// rows_per_patch: ny * nz when every patch of the run has the same nz (row
+// -> patch by division), else 0 (binary search over cell0)
+cudaError_t launch_dst_rows(int epi, const PatchDev* patches, int p0, int p1, long long c0, long long nrows, int nx,
+                            const double* qf, const unsigned char* active, double omega, const double* in,
+                            double* out, long long rows_per_patch, cudaStream_t s) {
   if (nrows <= 0) return cudaSuccess;
   if (nx > dst_max_nx()) return cudaErrorInvalidValue;
   DstRun R{patches, p0, p1, c0, nrows, nx, qf};
-  if (pro == kProRows && epi == kEpiStore) return dst_launch_k<kProRows, kEpiStore>(R, active, st, omega, in, out, s);
-  if (pro == kProResidual && epi == kEpiStore)
-    return dst_launch_k<kProResidual, kEpiStore>(R, active, st, omega, in, out, s);
-  if (pro == kProRows && epi == kEpiRelaxInPlace)
-    return dst_launch_k<kProRows, kEpiRelaxInPlace>(R, active, st, omega, in, out, s);
-  if (pro == kProRows && epi == kEpiRelaxInto)
-    return dst_launch_k<kProRows, kEpiRelaxInto>(R, active, st, omega, in, out, s);
+  if (epi == kEpiStore) return dst_launch_k<kEpiStore>(R, active, omega, in, out, rows_per_patch, s);
+  if (epi == kEpiRelaxInPlace) return dst_launch_k<kEpiRelaxInPlace>(R, active, omega, in, out, rows_per_patch, s);
+  if (epi == kEpiRelaxInto) return dst_launch_k<kEpiRelaxInto>(R, active, omega, in, out, rows_per_patch, s);
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_plane_gs_chain(const PlaneFac* d_fac, int nx, const PatchDev* patches, int p0, int np, int maxnz,
-                                  double czw, double* buf, cudaStream_t s) {
+static cudaError_t chain_smem_launch(const PlaneFac* d_fac, int nx, int ny, const PatchDev* patches, int p0, int np,
+                                    int maxnz, double czw, double* buf, int nj, cudaStream_t s) {
+  const int cpp = (nx + 63) / 64;
+  const size_t smem = (2 * (size_t)ny * 64 + (size_t)(ny - ny / 2) * 128 + 2 * (size_t)(nj + 1) * 64) * sizeof(double);
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e =
+      cudaFuncSetAttribute(plane_gs_chain_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  plane_gs_chain_smem_kernel<<<(unsigned)(np * cpp), 128, smem, s>>>(d_fac, patches, p0, cpp, maxnz, czw, buf, nj);
+  return cudaGetLastError();
+}
+
+// nj: rows from which the modal Thomas tables are bitwise constant (host
+// check in psm_plane_build), or -1 when they are not within the limit
+cudaError_t launch_plane_gs_chain(const PlaneFac* d_fac, int nx, int ny, int nj, const PatchDev* patches, int p0,
+                                  int np, int maxnz, double czw, double* buf, cudaStream_t s) {
   const long long nlines = (long long)np * nx;
   if (nlines == 0) return cudaSuccess;
+  // on-chip chains while their working set fits one SM (ny <= 128 at nj <= 48)
+  const size_t smem = (2 * (size_t)ny * 64 + (size_t)(ny - ny / 2) * 128 + 2 * (size_t)(nj + 1) * 64) * sizeof(double);
+  if (nj >= 0 && smem <= 220 * 1024 && !getenv("PSM_PLANE_CHAIN_GLOBAL"))
+    return chain_smem_launch(d_fac, nx, ny, patches, p0, np, maxnz, czw, buf, nj, s);
   plane_gs_chain_kernel<<<(unsigned)((2 * nlines + 127) / 128), 128, 0, s>>>(d_fac, patches, p0, nlines, maxnz, czw,
                                                                              buf);
   return cudaGetLastError();

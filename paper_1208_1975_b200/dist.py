@@ -292,12 +292,28 @@ def peer_halo(domain, dp):
     return domain._peer
 
 
-def jacobi_step_p2p(domain, dp, omega, slot, halo, step, events=None):
+def _timed(waits, device, fn):
+    """Run fn(); with a ``waits`` list, append the (start, end) CUDA events
+    bracketing the work it queues on the current stream."""
+    if waits is None:
+        return fn()
+    st = torch.cuda.current_stream(device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    out = fn()
+    b.record(st)
+    waits.append((a, b))
+    return out
+
+
+def jacobi_step_p2p(domain, dp, omega, slot, halo, step, events=None, waits=None):
     """One line-Jacobi step of a slab with the fused peer-memory halo (see
-    the module docstring).  ``step`` counts from 0 within the current run."""
+    the module docstring).  ``step`` counts from 0 within the current run.
+    ``waits``: optional list collecting the CUDA-event pair around the wait
+    for the neighbours' previous step (the halo stall of this rank)."""
     p = domain.patch
     stream = ctypes.c_void_p(torch.cuda.current_stream(p.device).cuda_stream)
-    halo.wait(halo.epoch + step, stream)
+    _timed(waits, p.device, lambda: halo.wait(halo.epoch + step, stream))
     if events is not None:
         a = torch.cuda.Event(enable_timing=True)
         a.record(torch.cuda.current_stream(p.device))
@@ -382,11 +398,12 @@ def dist_smooth(domain, config, cache, record_history=True):
         return [math.sqrt(v) for v in out.cpu().tolist()]
 
 
-def jacobi_step_overlapped(domain, dp, omega, slot, events=None):
+def jacobi_step_overlapped(domain, dp, omega, slot, events=None, waits=None):
     """One line-Jacobi step of a slab with the halo exchange overlapped with
     the interior sweep (see the module docstring).  ``events``: optional list
     collecting one list of (start, end) CUDA-event pairs per step, around the
-    sweep launches only (kernel time, not the halo)."""
+    sweep launches only (kernel time, not the halo); ``waits``: the event
+    pair around the compute stream's wait for the exchange and the unpack."""
     lib = _lib.load()
     p = domain.patch
     nzl = domain.nz_local
@@ -421,8 +438,12 @@ def jacobi_step_overlapped(domain, dp, omega, slot, events=None):
     sweep(1, nzl - 1)
     p.swap_buffers()
     dp.refresh(_lib.GHOST_ALL | _lib.GHOST_SKIP_X)
-    domain.finish_exchange(reqs)
-    domain.unpack(dp)
+
+    def land():
+        domain.finish_exchange(reqs)
+        domain.unpack(dp)
+
+    _timed(waits, p.device, land)
 
 
 # ---------------------------------------------------------------------------

@@ -149,3 +149,45 @@ def test_chaotic_gs_factor_general_line_length():
     for s in range(1, len(want)):
         got_f, ref_f = hist[s] / hist[s - 1], want[s] / want[s - 1]
         assert abs(got_f - ref_f) / ref_f < 0.02, (s, got_f, ref_f)
+
+
+# ---- multi-sweep mode (one launch runs every step of smooth(); single patch,
+# physical faces): sweep s+1 trails sweep s inside the launch ----------------
+@pytest.mark.parametrize("shape,steps", [((256, 24, 20), 5), ((128, 30, 7), 4), ((64, 9, 15), 6), ((72, 11, 8), 3),
+                                         ((32, 1, 9), 3), ((64, 12, 1), 3), ((256, 5, 8), 2)])
+def test_multisweep_wavefront_matches_serial(shape, steps):
+    o, g = _pair([(shape, (0, 0, 0))], seed=40 + sum(shape))
+    want, hist = _run(o, g, steps=steps)
+    assert G.rel_maxnorm(g.patches[0].u.cpu().numpy(), o.patches[0].u) < TOL
+    assert G.hist_rel(hist, want) < TOL
+
+
+def test_multisweep_nonunit_stencil():
+    center, faces = 6.5, (-1.2, -0.8, -1.0, -1.1, -0.9, -1.05)
+    o, g = _pair([((128, 14, 16), (0, 0, 0))], seed=8, center=center, faces=faces)
+    want, hist = _run(o, g, steps=4, omega=0.9, center=center, faces=faces)
+    assert G.rel_maxnorm(g.patches[0].u.cpu().numpy(), o.patches[0].u) < TOL
+    assert G.hist_rel(hist, want) < TOL
+
+
+def test_multisweep_chaotic_factor():
+    o, g = _pair([((256, 48, 40), (0, 0, 0))], seed=12)
+    want, hist = _run(o, g, steps=8, mode="chaotic")
+    for s in range(1, len(want)):
+        got_f, ref_f = hist[s] / hist[s - 1], want[s] / want[s - 1]
+        assert abs(got_f - ref_f) / ref_f < 0.02, (s, got_f, ref_f)
+
+
+def test_multisweep_equals_step_by_step():
+    """smooth() (graph, one multi-sweep launch) vs the eager per-step path
+    (timers): identical iterates; histories to rounding (the in-kernel
+    residual sums group the cells differently)."""
+    shape = (128, 20, 18)
+    a = _pair([(shape, (0, 0, 0))], seed=2)[1]
+    b = _pair([(shape, (0, 0, 0))], seed=2)[1]
+    cfg = ps.SmootherConfig(scheme="chaotic_block_gs", block_dims=(128, 1, 1), steps=6,
+                            strategy=ps.ExecutionStrategy.device(gs_mode="wavefront"))
+    _, ha = ps.smooth(a, cfg, ps.InverseCache())
+    _, hb = ps.smooth(b, cfg, ps.InverseCache(), {})
+    assert torch.equal(a.patches[0].u, b.patches[0].u)
+    assert max(abs(x - y) / y for x, y in zip(ha, hb)) < 1e-14

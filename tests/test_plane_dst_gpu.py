@@ -74,7 +74,7 @@ def test_plane_gs_single_patch(shape):
 def test_plane_gs_mixed_odd_even_patches():
     """9^3 before 16^3: the 16^3 patch's workspace offset (cell0 = 729) is odd,
     so its planes are only 8-byte aligned (advisor finding, round 1)."""
-    so = [((9, 9, 9), (0, 0, 0)), ((16, 16, 16), (9, 0, 0)), ((16, 16, 16), (0, 9, 0)), ((9, 9, 9), (25, 0, 0))]
+    so = [((9, 9, 9), (0, 0, 0)), ((16, 16, 16), (9, 0, 0)), ((16, 16, 16), (0, 16, 0)), ((9, 9, 9), (25, 0, 0))]
     o, g = _pair(so, seed=3)
     want = R.smooth(o, "chaotic_block_gs", (16, 16, 1), steps=2, exact_norm=False)
     cfg = ps.SmootherConfig(scheme="chaotic_block_gs", block_dims=(16, 16, 1), steps=2)

@@ -25,6 +25,8 @@ if len(rr) > 2:
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 sr = list(csv.reader(io.StringIO(src)))
 hdr = sr[1]; data = sr[2:]
+if "Warp Stall Sampling (All Samples)" not in hdr:
+    sys.exit(0)
 iS = hdr.index("Warp Stall Sampling (All Samples)"); iI = hdr.index("Instructions Executed")
 ts = sum(float(r[iS] or 0) for r in data); ti = sum(float(r[iI] or 0) for r in data)
 byop = collections.Counter(); bys = collections.Counter()
