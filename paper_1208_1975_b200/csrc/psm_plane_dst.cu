@@ -41,7 +41,7 @@ namespace psm {
 
 constexpr int kDstRows = 32;
 constexpr int kDstThreads = 256;
-constexpr int kDstNG = 4;   // n-tiles accumulated at a time
+constexpr int kDstNG = 4;   // n-tile granularity of the split table (the kernel accumulates NG = 4 or 8 at a time)
 
 // shared-memory geometry for row length nx
 struct DstGeom {
@@ -118,7 +118,7 @@ constexpr int kDstConsumers = 256;
 constexpr int kDstAllThreads = kDstConsumers + 32;
 constexpr int kDstStages = 3;
 
-template <int KSM, int EPI, bool QSM, bool BULK>
+template <int KSM, int EPI, bool QSM, bool BULK, int NG>
 __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRun R, const unsigned char* __restrict__ active,
                                                                      double omega, const double* __restrict__ in,
                                                                      double* __restrict__ out, int nstage, int ustaged,
@@ -242,15 +242,15 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
       // output (row, m = 8 nt + 2 (lane&3) + c) of parity par is x = 2 m + par
       double* orow = st + arow_i * G.ld + par;
       const int cnt = par ? half : nx - half;  // outputs of this parity
-      for (int n0 = 0; n0 < G.nt; n0 += kDstNG) {
-        double acc[kDstNG][2];
+      for (int n0 = 0; n0 < G.nt; n0 += NG) {
+        double acc[NG][2];
 #pragma unroll
-        for (int q = 0; q < kDstNG; ++q) acc[q][0] = acc[q][1] = 0.0;
+        for (int q = 0; q < NG; ++q) acc[q][0] = acc[q][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KSM; ++ks) {
           if (ks < G.ks) {
 #pragma unroll
-            for (int q = 0; q < kDstNG; ++q) {
+            for (int q = 0; q < NG; ++q) {
               const size_t o = ((size_t)ks * G.nt + n0 + q) * 32;
               const double b = QSM ? qb[o] : __ldg(qb + o);
               dmma884(acc[q][0], acc[q][1], a[ks], b);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
           }
         }
 #pragma unroll
-        for (int q = 0; q < kDstNG; ++q) {
+        for (int q = 0; q < NG; ++q) {
           const int m = 8 * (n0 + q) + 2 * (lane & 3);
           if (m < cnt) orow[2 * m] = acc[q][0];
           if (m + 1 < cnt) orow[2 * m + 2] = acc[q][1];
@@ -442,14 +442,27 @@ __global__ void __launch_bounds__(128, 1) plane_gs_chain_smem_kernel(const Plane
     async::cp_wait<1>();  // plane k (this thread's own copies) landed
     const double* S = stg + (size_t)(k & 1) * ny * 64 + q + row0 * 64;
     const bool act = valid && k < nz;
+    const double cz = k > 0 ? czw : 0.0;  // xhat(-1) = 0: X starts zeroed
     double prev = 0.0;
     if (act) {
+      // rows below nj use their own factors, the rest the converged ones
+      const int jn = min(len, nj);
+      const int sstep = drow * 64;
+      const double* sp = S;
+      double* xp = X;
+      const double* fp = finq;
+#pragma unroll 4
+      for (int jj = 0; jj < jn; ++jj, sp += sstep, xp += 128, fp += 64) {
+        const double v = fma(-cz, *xp, *sp);
+        prev = fma(-lo, prev, v) * *fp;
+        *xp = prev;
+      }
+      const double finf = finq[nj * 64];
 #pragma unroll 8
-      for (int jj = 0; jj < len; ++jj) {
-        double v = S[jj * drow * 64];
-        if (k > 0) v = fma(-czw, X[jj * 128], v);
-        prev = fma(-lo, prev, v) * finq[min(jj, nj) * 64];
-        X[jj * 128] = prev;
+      for (int jj = jn; jj < len; ++jj, sp += sstep, xp += 128) {
+        const double v = fma(-cz, *xp, *sp);
+        prev = fma(-lo, prev, v) * finf;
+        *xp = prev;
       }
     }
     const double y_oth = __shfl_xor_sync(0xffffffffu, prev, 1);
@@ -459,14 +472,29 @@ __global__ void __launch_bounds__(128, 1) plane_gs_chain_smem_kernel(const Plane
       const double cT = bot ? c_oth : c_own, cB = bot ? c_own : c_oth;
       const double xT = (yT - cT * yB) / (1.0 - cT * cB);
       double next = bot ? yB - cB * xT : xT;
-      double* dst = buf + P.cell0 + (long long)k * plane_cells + i + (long long)row0 * nx;
-      X[(len - 1) * 128] = next;
-      dst[(long long)(len - 1) * drow * nx] = next;
+      const long long dstep = (long long)drow * nx;
+      double* dp = buf + P.cell0 + (long long)k * plane_cells + i + (long long)row0 * nx + (len - 1) * dstep;
+      double* xp = X + (len - 1) * 128;
+      *xp = next;
+      *dp = next;
+      int jj = len - 2;
+      const double cinf = fcpq[nj * 64];
 #pragma unroll 8
-      for (int jj = len - 2; jj >= 0; --jj) {
-        next = fma(-fcpq[min(jj, nj) * 64], next, X[jj * 128]);
-        X[jj * 128] = next;
-        dst[(long long)jj * drow * nx] = next;
+      for (; jj >= nj; --jj) {
+        xp -= 128;
+        dp -= dstep;
+        next = fma(-cinf, next, *xp);
+        *xp = next;
+        *dp = next;
+      }
+      const double* fp = fcpq + jj * 64;
+#pragma unroll 4
+      for (; jj >= 0; --jj, fp -= 64) {
+        xp -= 128;
+        dp -= dstep;
+        next = fma(-*fp, next, *xp);
+        *xp = next;
+        *dp = next;
       }
     }
   }
@@ -496,13 +524,13 @@ void dst_split_table(const std::vector<double>& Q, int nx, std::vector<double>& 
 
 size_t dst_table_doubles(int nx) { return dst_geom(nx).qdoubles; }
 
-template <int KSM, int EPI, bool QSM, bool BULK>
+template <int KSM, int EPI, bool QSM, bool BULK, int NG>
 static cudaError_t dst_launch_t(const DstRun& R, const unsigned char* active, double omega, const double* in,
                                 double* out, int nstage, int ustaged, long long rpp, cudaStream_t s) {
   const bool us = EPI != kEpiStore && ustaged;
   const DstSmem M = dst_smem(R.nx, QSM, us, nstage);
   const size_t smem = M.total(us) * sizeof(double);
-  auto kern = dst_tile_kernel<KSM, EPI, QSM, BULK>;
+  auto kern = dst_tile_kernel<KSM, EPI, QSM, BULK, NG>;
   // the opt-in is per device and this size depends on nx: set it per launch
   // (host-side, no stream work)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -537,17 +565,25 @@ static cudaError_t dst_launch_k(const DstRun& R, const unsigned char* active, do
   if (!fits()) return cudaErrorInvalidValue;
   // bulk copies need 16-byte aligned rows: even nx and an even workspace offset
   const bool bulk = (R.nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
-#define PSM_DST(K_)                                                                                   \
-  if (qsm)                                                                                            \
-    return bulk ? dst_launch_t<K_, EPI, true, true>(R, active, omega, in, out, nstage, ustaged, rpp, s)     \
-                : dst_launch_t<K_, EPI, true, false>(R, active, omega, in, out, nstage, ustaged, rpp, s);   \
-  return bulk ? dst_launch_t<K_, EPI, false, true>(R, active, omega, in, out, nstage, ustaged, rpp, s)      \
-              : dst_launch_t<K_, EPI, false, false>(R, active, omega, in, out, nstage, ustaged, rpp, s)
+  // eight independent DMMA accumulator chains per warp when the n-tiles
+  // come in eights, else four
+  const bool ng8 = G.nt % 8 == 0;
+#define PSM_DST_NG(K_, Q_, B_) \
+  return ng8 ? dst_launch_t<K_, EPI, Q_, B_, 8>(R, active, omega, in, out, nstage, ustaged, rpp, s) \
+             : dst_launch_t<K_, EPI, Q_, B_, 4>(R, active, omega, in, out, nstage, ustaged, rpp, s)
+#define PSM_DST(K_)                        \
+  if (qsm) {                               \
+    if (bulk) PSM_DST_NG(K_, true, true);  \
+    PSM_DST_NG(K_, true, false);           \
+  }                                        \
+  if (bulk) PSM_DST_NG(K_, false, true);   \
+  PSM_DST_NG(K_, false, false)
   if (G.ks <= 8) { PSM_DST(8); }
   if (G.ks <= 16) { PSM_DST(16); }
   if (G.ks <= 32) { PSM_DST(32); }
   PSM_DST(64);
 #undef PSM_DST
+#undef PSM_DST_NG
 }
 
 // rows -> transformed rows (EPI store), or relaxed into the patches
