@@ -36,9 +36,6 @@ cudaError_t launch_line_zgen(const int* nxs, int nnx, int unit, const PatchDev* 
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
                            cudaStream_t stream);
-cudaError_t launch_line_jacobi_multi(const PatchDev* patches, int act0, const StencilDev& st, double omega, int steps,
-                                     double* partials, long long stride, long long ntiles, unsigned* bar, int threads,
-                                     size_t smem, cudaStream_t stream);
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
                                    long long max_face, int skip_x, int use_covered, cudaStream_t stream);
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
@@ -515,7 +512,6 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_unit_plane);
   cudaFree(P->d_gsflags);
   cudaFree(P->d_msflags);
-  cudaFree(P->d_gridbar);
   cudaFree(P->d_boxes);
   cudaFree(P->d_box_regions);
   psm_gs_pipe_free(P);
@@ -1078,37 +1074,6 @@ long long psm_plan_launches(const psm_plan* P) { return P ? P->launches : -1; }
 // history slot, all patches swap, refresh with the x faces skipped) [, final
 // residual]; GS: [refresh, residual] then steps x (sweep, refresh [,
 // residual]).  `act` is updated to the active flags after the steps.
-// Line Jacobi on one small patch with physical faces (L2-resident, the
-// launch-bound case): every step in one persistent launch with grid barriers
-// (line_jacobi_multi_kernel, psm_line.cu); 0 when the plan does not qualify
-static int jacobi_multi_steps(psm_plan* P, std::vector<unsigned char>& act, double omega, int steps, int history,
-                              cudaStream_t s, int* done) {
-  *done = 0;
-  if (P->kind != PSM_BLOCK_LINE || steps < 2 || !P->tiled || P->npatch != 1 || P->ncopy != 0) return PSM_OK;
-  const char* env = getenv("PSM_JACOBI_MULTI");
-  if (env && env[0] == '0') return PSM_OK;
-  const PatchDev& h = P->hp[0];
-  if (h.iface || h.peer_lo[0] || h.peer_hi[0]) return PSM_OK;
-  if ((long long)h.nx * h.ny * h.nz > (1LL << 22)) return PSM_OK;  // larger grids: the streaming kernels
-  unsigned char* da;
-  int rc = get_active(P, act.data(), &da);
-  if (rc) return rc;
-  if (!P->d_gridbar) CUDA_TRY(cudaMalloc(&P->d_gridbar, sizeof(unsigned)));
-  CUDA_TRY(cudaMemsetAsync(P->d_gridbar, 0, sizeof(unsigned), s));
-  double* part = nullptr;
-  if (history) {
-    part = slot_ptr(P, 0, &rc);
-    if (rc) return rc;
-  }
-  CUDA_TRY(launch_line_jacobi_multi(P->d_patches, act[0], P->st, omega, steps, part, std::max<long long>(1, P->ntiles),
-                                    P->ntiles, P->d_gridbar, P->threads, P->smem, s));
-  P->launches += 1;
-  if (steps & 1) act[0] ^= 1;
-  P->phys_pending = 0;  // every sweep wrote all physical ghosts of its buffer
-  *done = 1;
-  return PSM_OK;
-}
-
 // Line GS on one patch with physical faces: several steps per launch (the
 // multi-sweep mode of the pipelined kernel, psm_line_gs_pipe.cu); 0 when the
 // plan does not qualify (the caller then runs step by step)
@@ -1162,10 +1127,6 @@ static int smooth_sequence(psm_plan* P, std::vector<unsigned char>& act, int sch
     if (rc) return rc;
   }
   if (scheme == 0) {
-    int done = 0;
-    rc = jacobi_multi_steps(P, act, omega, steps, history, (cudaStream_t)stream, &done);
-    if (rc) return rc;
-    if (done) return PSM_OK;  // history slots 0..steps written by the launch
     for (int s = 0; s < steps; ++s) {
       rc = psm_jacobi_sweep(P, act.data(), omega, history ? s : -1, stream);
       if (rc) return rc;

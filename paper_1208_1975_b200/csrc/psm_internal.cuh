@@ -249,7 +249,6 @@ struct psm_plan {
   int gs_ntickets = 0;
   int* d_msflags = nullptr;   // multi-sweep line GS: steps * nplanes progress words + tickets
   long long ms_flag_cap = 0;
-  unsigned* d_gridbar = nullptr;  // multi-sweep line Jacobi: grid barrier counter
   // physical ghosts the sweeps since the last refresh left to it: 0 none
   // (one-tile / generic line-Jacobi kernels: written in their epilogues), 1
   // the y/z faces (z-marching line Jacobi, plane and box Jacobi: x faces

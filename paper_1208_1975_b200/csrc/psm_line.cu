@@ -23,22 +23,15 @@ namespace psm {
 
 constexpr int kMaxE = 8;  // cells per thread per tile
 
-// Field loads of the tile body: the read-only path in single-sweep launches;
-// L2-coherent loads (ld.global.cg) in the multi-sweep launch, where u was
-// written by other CTAs earlier in the same kernel
-template <bool CG>
-__device__ __forceinline__ double fld(const double* p) {
-  return CG ? __ldcg(p) : __ldg(p);
-}
-
-// One tile (R consecutive x-lines of one z-plane) of the sweep / residual;
-// act >= 0 overrides the active-buffer table.  Ends with the CTA in sync.
-template <int MODE, bool CG>  // MODE 0: residual partials only, 1: Jacobi sweep, 2: residual to rbuf (plane path)
-__device__ __forceinline__ void line_tile_body(const PatchDev* __restrict__ patches, int npatch,
-                                               const unsigned char* __restrict__ active, int act_override,
-                                               StencilDev st, double omega, double* __restrict__ partials,
-                                               double* __restrict__ rbuf, long long tile, double* sm, double* wsum) {
+template <int MODE>  // 0: residual partials only, 1: Jacobi sweep, 2: residual to rbuf (plane path)
+__global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __restrict__ patches, int npatch,
+                                                        const unsigned char* __restrict__ active, StencilDev st,
+                                                        double omega, double* __restrict__ partials,
+                                                        double* __restrict__ rbuf, long long tile_base) {
+  extern __shared__ double sm[];
+  __shared__ double wsum[32];
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31;
+  const long long tile = tile_base + blockIdx.x;
   const int pi = find_patch(patches, npatch, tile);
   const PatchDev& P = patches[pi];
   const int nx = P.nx, ny = P.ny;
@@ -47,7 +40,7 @@ __device__ __forceinline__ void line_tile_body(const PatchDev* __restrict__ patc
   int k, j0, R;
   tile_coords(P, tile, k, j0, R);
   const long long px = nx + 2, pxy = px * (ny + 2);
-  const int act = act_override >= 0 ? act_override : active[pi];
+  const int act = active[pi];
   const double* __restrict__ u = P.buf[act];
   double* __restrict__ v = P.buf[act ^ 1];
   const double* __restrict__ f = P.f;
@@ -73,11 +66,11 @@ __device__ __forceinline__ void line_tile_body(const PatchDev* __restrict__ patc
       xr[q] = ok[q] ? e - rr[q] * nx : 0;
       const long long iu = ubase + (long long)rr[q] * px + xr[q];
       if (ok[q]) {
-        c[q] = fld<CG>(u + iu);
-        ym[q] = fld<CG>(u + iu - px);
-        yp[q] = fld<CG>(u + iu + px);
-        zm[q] = fld<CG>(u + iu - pxy);
-        zp[q] = fld<CG>(u + iu + pxy);
+        c[q] = __ldg(u + iu);
+        ym[q] = __ldg(u + iu - px);
+        yp[q] = __ldg(u + iu + px);
+        zm[q] = __ldg(u + iu - pxy);
+        zp[q] = __ldg(u + iu + pxy);
         fv[q] = __ldg(f + fbase + e);
       } else {
         c[q] = ym[q] = yp[q] = zm[q] = zp[q] = fv[q] = 0.0;
@@ -90,8 +83,8 @@ __device__ __forceinline__ void line_tile_body(const PatchDev* __restrict__ patc
       ucen[h + q] = c[q];
       if (ok[q]) {
         const long long iu = ubase + (long long)rr[q] * px + xr[q];
-        if (lane == 0 || xr[q] == 0) xl = fld<CG>(u + iu - 1);
-        if (lane == 31 || xr[q] == nx - 1) xp_ = fld<CG>(u + iu + 1);
+        if (lane == 0 || xr[q] == 0) xl = __ldg(u + iu - 1);
+        if (lane == 31 || xr[q] == nx - 1) xp_ = __ldg(u + iu + 1);
         const double res = residual7(st, fv[q], c[q], xl, xp_, ym[q], yp[q], zm[q], zp[q]);
         ssq = fma(res, res, ssq);
         if (MODE == 1) rs[rr[q] * RS + xr[q] + (xr[q] >> 5)] = res;
@@ -109,10 +102,7 @@ __device__ __forceinline__ void line_tile_body(const PatchDev* __restrict__ patc
     for (int w = 0; w < (T >> 5); ++w) s += wsum[w];
     partials[tile] = s;
   }
-  if (MODE != 1) {
-    __syncthreads();  // wsum is reused by the next tile
-    return;
-  }
+  if (MODE != 1) return;
 
   // ---- B: local segment solves -------------------------------------------
   const int nseg = L->nseg, tail = L->tail;
@@ -184,58 +174,6 @@ __device__ __forceinline__ void line_tile_body(const PatchDev* __restrict__ patc
       }
     }
   }
-  __syncthreads();  // rs / ex are reused by the next tile
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(256, 2) line_tile_kernel(const PatchDev* __restrict__ patches, int npatch,
-                                                        const unsigned char* __restrict__ active, StencilDev st,
-                                                        double omega, double* __restrict__ partials,
-                                                        double* __restrict__ rbuf, long long tile_base) {
-  extern __shared__ double sm[];
-  __shared__ double wsum[32];
-  line_tile_body<MODE, false>(patches, npatch, active, -1, st, omega, partials, rbuf, tile_base + blockIdx.x, sm,
-                              wsum);
-}
-
-// Several line-Jacobi steps in one persistent launch (one patch, physical
-// faces, small enough to stay in L2: the launch-bound case, BASELINE C1).
-// Every sweep also writes v's physical ghosts (x faces and, fused, the y/z
-// faces), so after a grid-wide barrier the next sweep reads a fully
-// refreshed buffer; the history partials of sweep s (residual of u^s) land
-// in slot s, a last pass adds the residual of the final iterate in slot
-// `steps`.  The grid barrier is a monotone arrival counter (zeroed by the
-// host) that every CTA's thread 0 increments and polls with acquire loads;
-// all CTAs are co-resident (the host sizes the grid by occupancy).
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(256, 2) line_jacobi_multi_kernel(const PatchDev* __restrict__ patches, int act0,
-                                                                StencilDev st, double omega, int steps,
-                                                                double* __restrict__ partials, long long stride,
-                                                                long long ntiles, unsigned* bar) {
-  extern __shared__ double sm[];
-  __shared__ double wsum[32];
-  for (int s = 0; s < steps; ++s) {
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x)
-      line_tile_body<1, true>(patches, 1, nullptr, act0 ^ (s & 1), st, omega, partials ? partials + s * stride : nullptr,
-                              nullptr, t, sm, wsum);
-    grid_barrier(bar, (unsigned)(s + 1) * gridDim.x);
-  }
-  if (partials)
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x)
-      line_tile_body<0, true>(patches, 1, nullptr, act0 ^ (steps & 1), st, 0.0, partials + steps * stride, nullptr,
-                              t, sm, wsum);
 }
 
 // Generic exact line sweep: one thread per x-line, full-length Thomas with
@@ -580,23 +518,4 @@ cudaError_t line_tile_kernel_setup(size_t smem) {
   return cudaFuncSetAttribute(line_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-}  // namespace psm
-
-namespace psm {
-// launch geometry: all CTAs co-resident (the grid barrier needs it)
-cudaError_t launch_line_jacobi_multi(const PatchDev* patches, int act0, const StencilDev& st, double omega, int steps,
-                                     double* partials, long long stride, long long ntiles, unsigned* bar, int threads,
-                                     size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(line_jacobi_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, line_jacobi_multi_kernel, threads, smem);
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  const long long grid = std::min<long long>(ntiles, (long long)occ * sms);
-  line_jacobi_multi_kernel<<<(unsigned)grid, threads, smem, stream>>>(patches, act0, st, omega, steps, partials,
-                                                                      stride, ntiles, bar);
-  return cudaGetLastError();
-}
 }  // namespace psm
