@@ -93,7 +93,8 @@ int psm_box_build(const psm_stencil* st, int ex, int ey, int ez, psm_factors* F)
 namespace psm {
 cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                              double omega, const int4* blocks, int nblocks, int inplace, int mx, int my, int mz,
-                             int bx, int by, int bz, cudaStream_t s);
+                             int bx, int by, int bz, cudaStream_t s, const int4* gsdep = nullptr,
+                             int* flags = nullptr, int* ticket = nullptr);
 cudaError_t launch_box_apply(const BoxFac* F, const double* r, double* x, long long count, cudaStream_t s);
 }
 extern int psm_plane_band_mode;  // psm_plane.cu
@@ -435,7 +436,10 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     return fail(PSM_ECUDA, "plan setup: %s", cudaGetErrorString(err));
   }
   if (kind == PSM_BLOCK_BOX) {  // block list, wavefront-major (bi + bj + bk), then patch, then lexicographic
-    std::vector<std::vector<int>> waves;
+    // with each block's GS dependencies: its flag index (patch-major
+    // lexicographic numbering) and those of its -x, -y, -z neighbour blocks
+    std::vector<std::vector<int>> waves, wdeps;
+    int fbase = 0;
     for (int p = 0; p < npatch; ++p) {
       const psm_factors* F = P->fac[p];
       const PatchDev& h = P->hp[p];
@@ -444,14 +448,21 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
         for (int bj = 0; bj < cy; ++bj)
           for (int bi = 0; bi < cx; ++bi) {
             const int w = bi + bj + bk;
-            if ((int)waves.size() <= w) waves.resize(w + 1);
+            if ((int)waves.size() <= w) {
+              waves.resize(w + 1);
+              wdeps.resize(w + 1);
+            }
             waves[w].insert(waves[w].end(), {p, bi * F->nx, bj * F->ny, bk * F->nz});
+            const int id = fbase + bi + cx * (bj + cy * bk);
+            wdeps[w].insert(wdeps[w].end(), {id, bi > 0 ? id - 1 : -1, bj > 0 ? id - cx : -1, bk > 0 ? id - cx * cy : -1});
           }
+      fbase += cx * cy * cz;
     }
-    std::vector<int> all;
+    std::vector<int> all, deps;
     P->box_wave_off.assign(1, 0);
-    for (auto& w : waves) {
-      all.insert(all.end(), w.begin(), w.end());
+    for (size_t w = 0; w < waves.size(); ++w) {
+      all.insert(all.end(), waves[w].begin(), waves[w].end());
+      deps.insert(deps.end(), wdeps[w].begin(), wdeps[w].end());
       P->box_wave_off.push_back((int)(all.size() / 4));
     }
     P->nboxes = (int)(all.size() / 4);
@@ -479,6 +490,9 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     P->nregions = (int)(regs.size() / 4);
     cudaError_t e = cudaMalloc(&P->d_boxes, std::max<size_t>(16, all.size() * sizeof(int)));
     if (e == cudaSuccess) e = cudaMemcpy(P->d_boxes, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_box_deps, std::max<size_t>(16, deps.size() * sizeof(int)));
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_box_deps, deps.data(), deps.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_box_flags, (size_t)(P->nboxes + 1) * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&P->d_box_regions, std::max<size_t>(16, regs.size() * sizeof(int)));
     if (e == cudaSuccess)
       e = cudaMemcpy(P->d_box_regions, regs.data(), regs.size() * sizeof(int), cudaMemcpyHostToDevice);
@@ -514,6 +528,8 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_msflags);
   cudaFree(P->d_boxes);
   cudaFree(P->d_box_regions);
+  cudaFree(P->d_box_deps);
+  cudaFree(P->d_box_flags);
   psm_gs_pipe_free(P);
   for (auto& kv : P->unit_cache) cudaFree(kv.second.first);
   for (auto& kv : P->active_cache) cudaFree(kv.second);
@@ -1270,6 +1286,21 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
   P->phys_pending = 2;  // GS sweeps leave every physical ghost to the refresh
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_gs(P, da, omega, s);
   if (P->kind == PSM_BLOCK_BOX) {  // lexicographic block order = wavefronts bi+bj+bk, in place
+    // one persistent launch with per-block dependency flags when the blocks
+    // have template dims (psm_box.cu), else one launch per wavefront
+    const int bx = P->box_dims[0], by = P->box_dims[1], bz = P->box_dims[2];
+    const bool tmpl = (bx == 2 && by == 2 && bz == 2) || (bx == 4 && by == 2 && bz == 2) ||
+                      (bx == 4 && by == 4 && bz == 2) || (bx == 4 && by == 4 && bz == 4) ||
+                      (bx == 8 && by == 4 && bz == 4) || (bx == 8 && by == 8 && bz == 4) ||
+                      (bx == 8 && by == 8 && bz == 8);
+    const char* env = getenv("PSM_BOX_GS_WAVES");
+    if (tmpl && !(env && env[0] == '1')) {
+      CUDA_TRY(cudaMemsetAsync(P->d_box_flags, 0, (size_t)(P->nboxes + 1) * sizeof(int), s));
+      CUDA_TRY(launch_box_sweep(P->d_patches, da, P->st, omega, P->d_boxes, P->nboxes, 1, 1, 1, 1, bx, by, bz, s,
+                                P->d_box_deps, P->d_box_flags, P->d_box_flags + P->nboxes));
+      P->launches += 1;
+      return PSM_OK;
+    }
     for (size_t w = 0; w + 1 < P->box_wave_off.size(); ++w) {
       const int b0 = P->box_wave_off[w], b1 = P->box_wave_off[w + 1];
       CUDA_TRY(launch_box_sweep(P->d_patches, da, P->st, omega, P->d_boxes + b0, b1 - b0, 1, 1, 1, 1,

@@ -240,11 +240,25 @@ __device__ __forceinline__ void box_pass_mma(double* wc, int axis, const double 
 // fixed thread-to-cell/line mapping replaces the runtime integer divisions
 // that dominated the generic kernel's instruction count (ncu: 28% IMAD plus
 // software division).  Regions are clipped at patch edges at run time.
+// GS (gsdep != null): one persistent launch per sweep instead of one per
+// wavefront.  Blocks are handed out by an atomic ticket in wavefront order
+// (bi + bj + bk, the list the host built); a block waits until its three
+// lexicographic predecessors (gsdep[b].y/z/w: flag indices, -1 at patch
+// faces) have stored their new values, reads its halo (fresh: acquire fence,
+// no prefetch across dependent blocks), relaxes in place and releases its own
+// flag (gsdep[b].x).  Predecessors always hold smaller tickets, so the waits
+// cannot deadlock; the arithmetic is the lexicographic sweep's exactly.
+__device__ __forceinline__ int box_ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 template <int BX, int BY, int BZ, int MX, int MY, int MZ>
 __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restrict__ patches,
                                                      const unsigned char* __restrict__ active, StencilDev st,
                                                      double omega, const int4* __restrict__ blocks, int nblocks,
-                                                     int inplace) {
+                                                     int inplace, const int4* __restrict__ gsdep, int* flags,
+                                                     int* ticket) {
   constexpr int RX = BX * MX, RY = BY * MY, RZ = BZ * MZ;
   constexpr int HX = RX + 2, HY = RY + 2, HN = HX * HY * (RZ + 2);
   constexpr int NC = RX * RY * RZ;
@@ -295,14 +309,40 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
     }
     box_commit();
   };
-  stage(blockIdx.x, 0);
+  __shared__ int gs_b;
+  const bool gsp = gsdep != nullptr;
+  if (!gsp) stage(blockIdx.x, 0);
   int slot = 0;
   const BoxFac* afF = nullptr;  // factor object whose fragments af/scl hold
   double af[6][2], scl[4];
-  for (int b = blockIdx.x; b < nblocks; b += gridDim.x, slot ^= 1) {
-    stage(b + gridDim.x, slot ^ 1);
-    box_wait<1>();
-    __syncthreads();
+  for (int b = blockIdx.x;; b += gridDim.x, slot ^= 1) {
+    if (gsp) {
+      slot = 0;
+      if (tid == 0) {
+        const int tk = atomicAdd(ticket, 1);
+        if (tk < nblocks) {
+          const int4 d = gsdep[tk];
+          const int pred[3] = {d.y, d.z, d.w};
+          for (int q = 0; q < 3; ++q)
+            if (pred[q] >= 0)
+              while (box_ld_relaxed(flags + pred[q]) == 0) {
+              }
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        gs_b = tk;
+      }
+      __syncthreads();
+      b = gs_b;
+      if (b >= nblocks) break;
+      stage(b, 0);
+      box_wait<0>();
+      __syncthreads();
+    } else {
+      if (b >= nblocks) break;
+      stage(b + gridDim.x, slot ^ 1);
+      box_wait<1>();
+      __syncthreads();
+    }
     const double* hb = hbuf[slot];
     const double* fb = fbuf[slot];
     const int4 B = blocks[b];
@@ -448,6 +488,10 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
       }
     }
     __syncthreads();
+    if (gsp && tid == 0) {  // every thread's stores precede the barrier above: release them
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + gsdep[b].x), "r"(1) : "memory");
+    }
   }
 }
 
@@ -493,7 +537,7 @@ __global__ void __launch_bounds__(kBoxT) box_apply_kernel(const BoxFac* __restri
 // shapes of the reference's DEFAULT_BLOCK_SIZES get the compile-time kernel.
 cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                              double omega, const int4* blocks, int nblocks, int inplace, int mx, int my, int mz,
-                             int bx, int by, int bz, cudaStream_t s) {
+                             int bx, int by, int bz, cudaStream_t s, const int4* gsdep, int* flags, int* ticket) {
   if (nblocks <= 0) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -505,12 +549,13 @@ cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* activ
   if (bx == X && by == Y && bz == Z) {                                                                        \
     if (region) {                                                                                             \
       box_sweep_t<X, Y, Z, 8 / X, 8 / Y, 8 / Z><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks,    \
-                                                                      nblocks, inplace);                      \
+                                                                      nblocks, inplace, nullptr, nullptr,     \
+                                                                      nullptr);                               \
       return cudaGetLastError();                                                                              \
     }                                                                                                         \
     if (single) {                                                                                             \
       box_sweep_t<X, Y, Z, 1, 1, 1><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks, nblocks,       \
-                                                           inplace);                                          \
+                                                           inplace, gsdep, flags, ticket);                    \
       return cudaGetLastError();                                                                              \
     }                                                                                                         \
   }
