@@ -549,8 +549,7 @@ cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* activ
   if (bx == X && by == Y && bz == Z) {                                                                        \
     if (region) {                                                                                             \
       box_sweep_t<X, Y, Z, 8 / X, 8 / Y, 8 / Z><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks,    \
-                                                                      nblocks, inplace, nullptr, nullptr,     \
-                                                                      nullptr);                               \
+                                                                      nblocks, inplace, gsdep, flags, ticket); \
       return cudaGetLastError();                                                                              \
     }                                                                                                         \
     if (single) {                                                                                             \

@@ -30,8 +30,7 @@ void plane_band_tables(long double c, long double a, long double blo, long doubl
 int band_k_for(int nx);
 cudaError_t launch_plane_band_jacobi(int K, int BW, const PatchDev* patches, const unsigned char* active,
                                      double omega, const double* rbuf, double* zbuf, const int2* units,
-                                     int nunits, const double* hinf_host, const StencilDev& st, double* partials,
-                                     cudaStream_t s);
+                                     int nunits, const double* hinf_host, cudaStream_t s);
 void dst_split_table(const std::vector<double>& Q, int nx, std::vector<double>& out);
 size_t dst_table_doubles(int nx);
 int dst_max_nx();
@@ -471,11 +470,7 @@ static long long run_rows_per_patch(const psm_plan* P, const PlaneRun& r) {
 // back -> relax into v.
 int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double* partials, cudaStream_t s) {
   PlaneState* S = P->plane;
-  // every run banded: the band kernel forms the residual (and the history
-  // partials) itself; otherwise one residual pass feeds every run
-  bool all_band = psm_plane_band_mode != 0 && !getenv("PSM_BAND_UNFUSED");
-  for (const PlaneRun& r : S->runs) all_band = all_band && r.bw > 0;
-  if (!all_band) {
+  {
     const int rc = psm_plane_residual(P, da, partials, S->rbuf, s);
     if (rc) return rc;
   }
@@ -494,8 +489,8 @@ int psm_plane_jacobi(psm_plan* P, const unsigned char* da, double omega, double*
     }
     if (r.bw > 0 && psm_plane_band_mode != 0) {
       cudaStream_t rs = fan ? P->side[bi++ % psm_plan::kSide] : s;
-      PCUDA(launch_plane_band_jacobi(band_k_for(r.nx), r.bw, P->d_patches, da, omega, all_band ? nullptr : S->rbuf,
-                                     S->rhat, r.d_units, r.nunits, r.hinf.data(), P->st, partials, rs));
+      PCUDA(launch_plane_band_jacobi(band_k_for(r.nx), r.bw, P->d_patches, da, omega, S->rbuf, S->rhat, r.d_units,
+                                     r.nunits, r.hinf.data(), rs));
       P->launches += 1;
       continue;
     }

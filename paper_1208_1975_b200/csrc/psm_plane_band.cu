@@ -69,13 +69,7 @@ struct BandCfg {
   static constexpr int EXTP = EXT + EXT / K + 2;
   static constexpr int ROWP = NMAX + NMAX / K + 2;
   static constexpr int D = 2, P = D - 1;
-  // fused residual (FUSE): plane-k rows j-1..j+2 (padded, ghosts included)
-  // and rows j, j+1 of planes k-1, k+1 and f
-  static constexpr int UROW = NMAX + 2 + (NMAX & 1 ? 1 : 0) + 2;  // >= nx + 2, even
-  // (the k-1 / k+1 rows reuse ringA / ringB, idle in a fused forward sweep)
-  static constexpr int FUSE_DOUBLES = 4 * UROW + 2 * NMAX;
   static constexpr size_t SMEM = (size_t)(2 * EXTP + ROWP + 2 * D * NMAX) * sizeof(double);
-  static constexpr size_t SMEM_FUSE = (size_t)(2 * EXTP + ROWP + 2 * D * NMAX + FUSE_DOUBLES) * sizeof(double);
   __device__ static __forceinline__ int pos(int e) { return K > 1 ? e + e / K : e; }
 };
 
@@ -113,18 +107,13 @@ __device__ __forceinline__ void band_conv_row(const double* __restrict__ e, cons
   }
 }
 
-// FUSE: the forward sweep forms r_j = f - A u itself (reference order,
-// residual7) from streamed rows of u and f instead of reading a residual
-// buffer, and the plane's sum of r^2 (history partial of u) goes to the
-// plane's first line tile in `partials` (its other tiles get zero).
-template <int K, int BW, int FUSE>
+template <int K, int BW>
 __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel(const PatchDev* __restrict__ patches,
                                                                   const unsigned char* __restrict__ active,
                                                                   double omega, const double* __restrict__ rbuf,
                                                                   double* __restrict__ zbuf,
                                                                   const int2* __restrict__ units, int nunits,
-                                                                  const __grid_constant__ BandHinf Hinf,
-                                                                  StencilDev st, double* __restrict__ partials) {
+                                                                  const __grid_constant__ BandHinf Hinf) {
   using C = BandCfg<K, BW>;
   constexpr int NMAX = C::NMAX, EXTP = C::EXTP, D = C::D, P = C::P;
   extern __shared__ __align__(16) double bsm[];
@@ -132,11 +121,6 @@ __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel
   double* crow = ext + 2 * EXTP;      // [ROWP] convolution outputs (padded positions)
   double* ringA = crow + C::ROWP;     // [D][NMAX] r rows (forward) / z rows (backward)
   double* ringB = ringA + D * NMAX;   // [D][NMAX] u rows (backward)
-  double* fU = ringB + D * NMAX;       // FUSE: [4][UROW] plane-k rows (row r in slot (r+1)%4)
-  double* fZm = ringA;                 //       [2][NMAX] plane k-1 row, plane k+1 row (forward only), f row
-  double* fZp = ringB;
-  double* fF = fU + 4 * C::UROW;
-  __shared__ double bsum[kBandT / 32];
   const int t = threadIdx.x;
 
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
@@ -157,37 +141,8 @@ __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel
       ext[t * EXTP + C::pos(n + BW)] = 0.0;
     }
     // ---------------- forward: z_j = S_j^{-1}(r_j - b_lo z_{j-1}) ----------
-    const double* uk = Pd.buf[act] + (long long)(k + 1) * pxy;  // plane k, padded row 0 (ghost row j = -1)
-    const double* fkp = Pd.f + (long long)k * ny * n;
-    double ssq = 0.0;
-    auto issueU = [&](int r) {  // plane-k padded row r+1 (interior row r, -1 <= r <= ny)
-      if (r <= ny) {
-        double* dst = fU + ((r + 1) & 3) * C::UROW;
-        const double* src = uk + (long long)(r + 1) * px;
-        for (int p = t; p < n + 2; p += kBandT) band_cp8(dst + p, src + p);
-      }
-    };
-    auto issueZF = [&](int j) {  // row j of planes k-1, k+1 and of f
-      if (j < ny) {
-        const int sl = (j & 1) * NMAX;
-        const double* zm_src = uk - pxy + (long long)(j + 1) * px + 1;
-        const double* zp_src = uk + pxy + (long long)(j + 1) * px + 1;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          const int p = t + kBandT * i;
-          if (p < n) {
-            band_cp8(fZm + sl + p, zm_src + p);
-            band_cp8(fZp + sl + p, zp_src + p);
-            band_cp8(fF + sl + p, fkp + (long long)j * n + p);
-          }
-        }
-      }
-    };
     auto issueF = [&](int j) {
-      if (FUSE) {
-        issueU(j + 1);  // rows j-1, j were issued before; row j+1 completes the stencil of row j
-        issueZF(j);
-      } else if (j < ny) {
+      if (j < ny) {
         double* dst = ringA + (j % D) * NMAX;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -197,10 +152,6 @@ __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel
       }
       band_commit();
     };
-    if (FUSE) {
-      issueU(-1);
-      issueU(0);
-    }
 #pragma unroll
     for (int j = 0; j < P; ++j) issueF(j);
     for (int j = 0; j < ny; ++j) {
@@ -217,19 +168,7 @@ __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel
             zp = crow[C::pos(p)];
             __stcg(zk + (long long)(j - 1) * n + p, zp);
           }
-          double rv;
-          if (FUSE) {
-            const double* um = fU + (j & 3) * C::UROW;        // row j-1
-            const double* uc = fU + ((j + 1) & 3) * C::UROW;  // row j
-            const double* up = fU + ((j + 2) & 3) * C::UROW;  // row j+1
-            const int sl = (j & 1) * NMAX;
-            rv = residual7(st, fF[sl + p], uc[p + 1], uc[p], uc[p + 2], um[p + 1], up[p + 1], fZm[sl + p],
-                           fZp[sl + p]);
-            ssq = fma(rv, rv, ssq);
-          } else {
-            rv = ra[p];
-          }
-          const double tv = fma(-blo, zp, rv);
+          const double tv = fma(-blo, zp, ra[p]);
           e[C::pos(p + BW)] = tv;
           if (p <= BW - 2) e[C::pos(BW - 2 - p)] = -tv;
           if (p >= n - BW + 1) e[C::pos(2 * n - p + BW)] = -tv;
@@ -246,19 +185,6 @@ __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel
       __syncthreads();
     }
     band_wait<0>();
-    if (FUSE && partials) {  // the plane's sum of r^2: fixed warp tree, warps in order
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
-      if ((t & 31) == 0) bsum[t >> 5] = ssq;
-      __syncthreads();
-      double* slot = partials + Pd.tile0 + (long long)k * Pd.tpp;
-      for (int q = t; q < Pd.tpp; q += kBandT) {
-        double v = 0.0;
-        if (q == 0)
-          for (int w = 0; w < kBandT / 32; ++w) v += bsum[w];
-        slot[q] = v;
-      }
-    }
     __threadfence_block();  // z rows stored above are re-read below by the same threads
     // ---------------- backward: x_j = z_j - S_j^{-1}(b_up x_{j+1}) --------
     auto issueB = [&](int b) {  // backward step b handles row j = ny-1-b
@@ -321,19 +247,20 @@ __global__ void __launch_bounds__(kBandT, 384 / kBandT) plane_band_jacobi_kernel
   }
 }
 
-template <int K, int BW, int FUSE>
+template <int K, int BW>
 static cudaError_t band_launch_t(const PatchDev* patches, const unsigned char* active, double omega,
                                  const double* rbuf, double* zbuf, const int2* units, int nunits, int sms,
-                                 const BandHinf& Hinf, const StencilDev& st, double* partials, cudaStream_t s) {
+                                 const BandHinf& Hinf, cudaStream_t s) {
   using C = BandCfg<K, BW>;
-  constexpr size_t smem = FUSE ? C::SMEM_FUSE : C::SMEM;
-  auto kern = plane_band_jacobi_kernel<K, BW, FUSE>;
   static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr)) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(plane_band_jacobi_kernel<K, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  }
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBandT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plane_band_jacobi_kernel<K, BW>, kBandT, C::SMEM);
   const int grid = std::max(1, std::min(nunits, std::max(1, occ) * sms));
-  kern<<<grid, kBandT, smem, s>>>(patches, active, omega, rbuf, zbuf, units, nunits, Hinf, st, partials);
+  plane_band_jacobi_kernel<K, BW><<<grid, kBandT, C::SMEM, s>>>(patches, active, omega, rbuf, zbuf, units, nunits,
+                                                                Hinf);
   return cudaGetLastError();
 }
 
@@ -343,12 +270,9 @@ int band_k_for(int nx) {  // outputs per thread: kBandT * K >= nx
   return 0;
 }
 
-// rbuf null: the residual is formed in the kernel (FUSE) and the history
-// partials go to `partials`
 cudaError_t launch_plane_band_jacobi(int K, int BW, const PatchDev* patches, const unsigned char* active,
                                      double omega, const double* rbuf, double* zbuf, const int2* units,
-                                     int nunits, const double* hinf_host, const StencilDev& st, double* partials,
-                                     cudaStream_t s) {
+                                     int nunits, const double* hinf_host, cudaStream_t s) {
   if (nunits <= 0) return cudaSuccess;
   BandHinf Hinf;
   memset(&Hinf, 0, sizeof Hinf);
@@ -356,12 +280,8 @@ cudaError_t launch_plane_band_jacobi(int K, int BW, const PatchDev* patches, con
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#define PSM_BAND(KK, BB)                                                                                       \
-  if (K == KK && BW == BB)                                                                                     \
-    return rbuf ? band_launch_t<KK, BB, 0>(patches, active, omega, rbuf, zbuf, units, nunits, sms, Hinf, st,      \
-                                           partials, s)                                                          \
-                : band_launch_t<KK, BB, 1>(patches, active, omega, rbuf, zbuf, units, nunits, sms, Hinf, st,      \
-                                           partials, s);
+#define PSM_BAND(KK, BB) \
+  if (K == KK && BW == BB) return band_launch_t<KK, BB>(patches, active, omega, rbuf, zbuf, units, nunits, sms, Hinf, s);
 #define PSM_BAND_K(KK) PSM_BAND(KK, 16) PSM_BAND(KK, 32) PSM_BAND(KK, 48)
   PSM_BAND_K(1)
   PSM_BAND_K(2)
