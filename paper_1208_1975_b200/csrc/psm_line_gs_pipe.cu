@@ -973,12 +973,24 @@ int psm_gs_pipe_multi(psm_plan* P, const unsigned char* da, double omega, int ch
   const PatchDev& h = P->hp[0];
   auto it = S->ms_units.find(steps);
   if (it == S->ms_units.end()) {
-    std::vector<int> uv;
+    // ticket order: by k0 + (W+1) s, i.e. roughly the order in which units
+    // become ready (sweep s+1 trails sweep s by about one plane group), so
+    // CTAs do not sit on units far ahead of the wavefront.  Every unit a
+    // unit waits on -- (s, k0-W), (s-1, k0), (s-1, k0+W) -- has a strictly
+    // smaller key, so the order stays deadlock-free.
+    std::vector<std::pair<long long, int2>> order;
     for (int sw = 0; sw < steps; ++sw)
-      for (int k0 = 0; k0 < h.nz; k0 += kGsW) {
-        uv.push_back(sw << 16);
-        uv.push_back(k0);
-      }
+      for (int k0 = 0; k0 < h.nz; k0 += kGsW)
+        order.push_back({(long long)k0 + (long long)(kGsW + 1) * sw, make_int2(sw << 16, k0)});
+    std::stable_sort(order.begin(), order.end(),
+                     [](const std::pair<long long, int2>& a, const std::pair<long long, int2>& b) {
+                       return a.first < b.first;
+                     });
+    std::vector<int> uv;
+    for (auto& o : order) {
+      uv.push_back(o.second.x);
+      uv.push_back(o.second.y);
+    }
     int2* d = nullptr;
     if (cudaMalloc(&d, uv.size() * sizeof(int)) != cudaSuccess)
       return psm_set_error(PSM_ENOMEM, "cudaMalloc for multi-sweep GS units");

@@ -211,33 +211,46 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
   }
 
   // ============================== consumers ===================================
-  const int mt = warp & 3, par = warp >> 2;
-  int it = 0;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+  // Two groups of four warps take alternate tiles (ping-pong), so one
+  // group's A-load and epilogue phases overlap the other's MMA; warp w of a
+  // group owns the 8-row m-tile w of its tile, both parities.
+  constexpr int kGroupThreads = kDstConsumers / 2;
+  const int grp = warp >> 2, mt = warp & 3;
+  const int gtid = tid & (kGroupThreads - 1);
+  const int bar_id = 1 + grp;
+  int it = grp;
+  for (long long t = blockIdx.x + (long long)grp * gridDim.x; t < ntiles; t += 2LL * gridDim.x, it += 2) {
     const int s = it % nstage;
     async::bar_wait(&full[s], (it / nstage) & 1);
     double* st = stage(s);
     const int nvalid = (int)min((long long)kDstRows, R.nrows - t * kDstRows);
-    // ---- split DST: this warp's 8 rows x one parity ----------------------
-    // A fragments (pair sums / differences) for the whole K go to registers;
-    // after the barrier no warp reads the rows, so outputs overwrite them
+    // ---- split DST: this warp's 8 rows, both parities ---------------------
+    // A fragments (pair sums and differences) for the whole K go to
+    // registers; after the group barrier no warp of the group reads the rows,
+    // so outputs overwrite them in place
     const int arow_i = 8 * mt + (lane >> 2);
     const double* arow = st + arow_i * G.ld;
     const bool arow_ok = arow_i < nvalid;
-    const double sgn = par ? -1.0 : 1.0;
-    double a[KSM];
+    double a[2][KSM];
 #pragma unroll
     for (int q = 0; q < KSM; ++q) {
       const int p = 4 * q + (lane & 3);
-      double v = 0.0;
+      double e = 0.0, o = 0.0;
       if (arow_ok) {
-        if (p < half) v = arow[p] + sgn * arow[nx - 1 - p];
-        else if (p == mid && par == 0) v = arow[p];
+        if (p < half) {
+          const double l = arow[p], r = arow[nx - 1 - p];
+          e = l + r;
+          o = l - r;
+        } else if (p == mid) {
+          e = arow[p];
+        }
       }
-      a[q] = v;
+      a[0][q] = e;
+      a[1][q] = o;
     }
-    async::named_sync(1, kDstConsumers);
-    {
+    async::named_sync(bar_id, kGroupThreads);
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
       const double* qb = (QSM ? qs : R.qf) + (size_t)par * G.ks * G.nt * 32 + lane;
       // output (row, m = 8 nt + 2 (lane&3) + c) of parity par is x = 2 m + par
       double* orow = st + arow_i * G.ld + par;
@@ -252,8 +265,8 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
 #pragma unroll
             for (int q = 0; q < NG; ++q) {
               const size_t o = ((size_t)ks * G.nt + n0 + q) * 32;
-              const double b = QSM ? qb[o] : __ldg(qb + o);
-              dmma884(acc[q][0], acc[q][1], a[ks], b);
+              const double bb = QSM ? qb[o] : __ldg(qb + o);
+              dmma884(acc[q][0], acc[q][1], a[par][ks], bb);
             }
           }
         }
@@ -265,9 +278,9 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
         }
       }
     }
-    async::named_sync(1, kDstConsumers);
+    async::named_sync(bar_id, kGroupThreads);
     // ---- epilogue: coalesced row stores ---------------------------------
-    for (int r = warp; r < nvalid; r += kDstConsumers / 32) {
+    for (int r = mt; r < nvalid; r += 4) {
       const double* trow = st + r * G.ld;
       const long long g = t * kDstRows + r;
       if (EPI == kEpiStore) {
@@ -292,8 +305,8 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
         }
       }
     }
-    async::named_sync(1, kDstConsumers);  // every consumer is done with stage s
-    if (tid == 0) async::bar_arrive(&empty[s]);
+    async::named_sync(bar_id, kGroupThreads);  // the group is done with stage s
+    if (gtid == 0) async::bar_arrive(&empty[s]);
   }
 }
 
@@ -561,8 +574,7 @@ static cudaError_t dst_launch_k(const DstRun& R, const unsigned char* active, do
   if (!fits()) nstage = kDstStages;
   if (!fits()) nstage = 2;
   if (!fits()) ustaged = 0;
-  if (!fits()) nstage = 1;
-  if (!fits()) return cudaErrorInvalidValue;
+  if (!fits()) return cudaErrorInvalidValue;  // the two consumer groups need two stages
   // bulk copies need 16-byte aligned rows: even nx and an even workspace offset
   const bool bulk = (R.nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
   // eight independent DMMA accumulator chains per warp when the n-tiles

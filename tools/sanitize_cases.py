@@ -64,7 +64,41 @@ CASES = {
     "box_gs": lambda: run("box_gs", level([((12, 10, 9), (0, 0, 0))]), "chaotic_block_gs", (4, 4, 4)),
     "ghosts_lattice_jacobi": lambda: run("ghosts_lattice_jacobi", level(lattice((2, 2, 2), (16, 12, 10))),
                                          "block_jacobi", (16, 1, 1)),
+    # round 2: multi-sweep line GS (single patch, 4 steps in one launch)
+    "gs_multisweep": lambda: run("gs_multisweep", level([((64, 10, 16), (0, 0, 0))]), "chaotic_block_gs",
+                                 (64, 1, 1), steps=4),
+    # DST tiles + one-launch chain (plane GS), DST tiles in Jacobi ('dst' mode)
+    "plane_gs_dst_chain": lambda: run("plane_gs_dst_chain", level([((64, 48, 6), (0, 0, 0))]), "chaotic_block_gs",
+                                      (64, 48, 1), steps=2),
+    "plane_jacobi_dst": lambda: plane_dst_jacobi(),
+    # persistent box GS (dependency flags)
+    "box_gs_persistent": lambda: run("box_gs_persistent", level([((24, 16, 16), (0, 0, 0))]), "chaotic_block_gs",
+                                     (8, 8, 8)),
+    "api_primitives": lambda: api_primitives(),
 }
+
+
+def plane_dst_jacobi():
+    prev = ps.plane_solver("dst")
+    try:
+        run("plane_jacobi_dst", level([((40, 24, 5), (0, 0, 0))]), "block_jacobi", (40, 24, 1))
+    finally:
+        ps.plane_solver(prev)
+
+
+def api_primitives():
+    rng = np.random.default_rng(3)
+    p = ps.Patch(ps.PatchDims(9, 7, 6))
+    p.u.copy_(torch.from_numpy(rng.standard_normal(p.u.shape)))
+    st = ps.Stencil7()
+    ps.block_residual(st, p, ps.BlockRange((1, 2, 0), (8, 3, 6)))
+    ps.apply_stencil(st, p, (4, 3, 2))
+    m = rng.standard_normal((40, 40)) + 40 * np.eye(40)
+    ps.matvec(m, rng.standard_normal(40))
+    ps.block_update(rng.standard_normal(40), rng.standard_normal(40), m, 0.7)
+    ps.invert_dense(m)
+    torch.cuda.synchronize()
+    print("api_primitives: ok", flush=True)
 CHAOTIC = {
     "gs_pipe_chaotic": lambda: run("gs_pipe_chaotic", level(lattice((2, 1, 2), (64, 10, 9))), "chaotic_block_gs",
                                    (64, 1, 1), mode="chaotic"),
