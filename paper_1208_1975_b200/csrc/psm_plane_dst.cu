@@ -122,7 +122,7 @@ template <int KSM, int EPI, bool QSM, bool BULK, int NG>
 __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRun R, const unsigned char* __restrict__ active,
                                                                      double omega, const double* __restrict__ in,
                                                                      double* __restrict__ out, int nstage, int ustaged,
-                                                                     long long rows_per_patch) {
+                                                                     long long rows_per_patch, int pingpong) {
   constexpr bool RELAX = EPI != kEpiStore;
   extern __shared__ __align__(16) double dsm[];
   const int nx = R.nx;
@@ -214,12 +214,21 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
   // Two groups of four warps take alternate tiles (ping-pong), so one
   // group's A-load and epilogue phases overlap the other's MMA; warp w of a
   // group owns the 8-row m-tile w of its tile, both parities.
-  constexpr int kGroupThreads = kDstConsumers / 2;
-  const int grp = warp >> 2, mt = warp & 3;
+  // (PP: ping-pong, both parities per warp; large K keeps one group of eight
+  // warps, one parity each, to bound the A-fragment registers; one stage
+  // also means one group)
+  constexpr bool PPK = KSM <= 16;
+  const bool PP = PPK && pingpong && nstage >= 2;
+  const int ngrp = PP ? 2 : 1;
+  const int kGroupThreads = kDstConsumers / ngrp;
+  const int grp = PP ? warp >> 2 : 0;
+  const int mt = warp & 3;
+  const int par_lo = PP ? 0 : warp >> 2;
   const int gtid = tid & (kGroupThreads - 1);
   const int bar_id = 1 + grp;
   int it = grp;
-  for (long long t = blockIdx.x + (long long)grp * gridDim.x; t < ntiles; t += 2LL * gridDim.x, it += 2) {
+  for (long long t = blockIdx.x + (long long)grp * gridDim.x; t < ntiles; t += (long long)ngrp * gridDim.x,
+                 it += ngrp) {
     const int s = it % nstage;
     async::bar_wait(&full[s], (it / nstage) & 1);
     double* st = stage(s);
@@ -231,7 +240,8 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
     const int arow_i = 8 * mt + (lane >> 2);
     const double* arow = st + arow_i * G.ld;
     const bool arow_ok = arow_i < nvalid;
-    double a[2][KSM];
+    constexpr int NPA = PPK ? 2 : 1;  // parities whose A fragments this warp holds
+    double a[NPA][KSM];
 #pragma unroll
     for (int q = 0; q < KSM; ++q) {
       const int p = 4 * q + (lane & 3);
@@ -245,12 +255,20 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
           e = arow[p];
         }
       }
-      a[0][q] = e;
-      a[1][q] = o;
+      if (PPK) {
+        a[0][q] = e;
+        a[NPA - 1][q] = o;
+      } else {
+        a[0][q] = par_lo ? o : e;
+      }
     }
     async::named_sync(bar_id, kGroupThreads);
 #pragma unroll
-    for (int par = 0; par < 2; ++par) {
+    for (int ai = 0; ai < NPA; ++ai) {  // compile-time index into a[]
+      // PPK: a[0] even, a[1] odd; with one group (PP false) a warp runs only
+      // its own parity par_lo, whose fragments a[par_lo] (PPK) or a[0] hold
+      if (PPK && !PP && ai != par_lo) continue;
+      const int par = PPK ? ai : par_lo;
       const double* qb = (QSM ? qs : R.qf) + (size_t)par * G.ks * G.nt * 32 + lane;
       // output (row, m = 8 nt + 2 (lane&3) + c) of parity par is x = 2 m + par
       double* orow = st + arow_i * G.ld + par;
@@ -266,7 +284,7 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
             for (int q = 0; q < NG; ++q) {
               const size_t o = ((size_t)ks * G.nt + n0 + q) * 32;
               const double bb = QSM ? qb[o] : __ldg(qb + o);
-              dmma884(acc[q][0], acc[q][1], a[par][ks], bb);
+              dmma884(acc[q][0], acc[q][1], a[ai][ks], bb);
             }
           }
         }
@@ -280,7 +298,7 @@ __global__ void __launch_bounds__(kDstAllThreads, 1) dst_tile_kernel(const DstRu
     }
     async::named_sync(bar_id, kGroupThreads);
     // ---- epilogue: coalesced row stores ---------------------------------
-    for (int r = mt; r < nvalid; r += 4) {
+    for (int r = PP ? mt : warp; r < nvalid; r += PP ? 4 : 8) {
       const double* trow = st + r * G.ld;
       const long long g = t * kDstRows + r;
       if (EPI == kEpiStore) {
@@ -409,24 +427,26 @@ __global__ void __launch_bounds__(128) plane_gs_chain_kernel(const PlaneFac* __r
 // tables are bitwise constant from there on, checked on the host).  Global
 // traffic is one read and one write of every value.  One CTA = 64 modes of
 // one patch, two threads per mode.
-__global__ void __launch_bounds__(128, 1) plane_gs_chain_smem_kernel(const PlaneFac* __restrict__ F,
+template <int MPC>  // modes per CTA (two threads each)
+__global__ void __launch_bounds__(2 * MPC) plane_gs_chain_smem_kernel(const PlaneFac* __restrict__ F,
                                                                      const PatchDev* __restrict__ patches, int p0,
                                                                      int cpp, int maxnz, double czw,
                                                                      double* __restrict__ buf, int nj) {
   extern __shared__ __align__(16) double csm[];
   const int nx = F->nx, ny = F->ny, m = ny / 2, hmax = ny - m;
   const int tid = threadIdx.x, q = tid >> 1, bot = tid & 1;
-  const int pl = blockIdx.x / cpp, i0 = (blockIdx.x - pl * cpp) * 64;
+  const int pl = blockIdx.x / cpp, i0 = (blockIdx.x - pl * cpp) * MPC;
   const int i = i0 + q;
   const bool valid = i < nx;
   const PatchDev& P = patches[p0 + pl];
   const int nz = P.nz;
-  double* stg = csm;                              // [2][ny][64] transformed residuals
-  double* X = stg + 2 * (size_t)ny * 64 + tid;    // [hmax][128] this thread's column
-  double* fin = csm + 2 * (size_t)ny * 64 + (size_t)hmax * 128;  // [nj+1][64] 1/m
-  double* fcp = fin + (size_t)(nj + 1) * 64;                      // [nj+1][64] c'
-  for (int e = tid; e < (nj + 1) * 64; e += 128) {
-    const int jj = e >> 6, ii = i0 + (e & 63);
+  constexpr int T = 2 * MPC;
+  double* stg = csm;                               // [2][ny][MPC] transformed residuals
+  double* X = stg + 2 * (size_t)ny * MPC + tid;    // [hmax][T] this thread's column
+  double* fin = csm + 2 * (size_t)ny * MPC + (size_t)hmax * T;  // [nj+1][MPC] 1/m
+  double* fcp = fin + (size_t)(nj + 1) * MPC;                    // [nj+1][MPC] c'
+  for (int e = tid; e < (nj + 1) * MPC; e += T) {
+    const int jj = e / MPC, ii = i0 + (e % MPC);
     const long long o = (long long)jj * nx + ii;
     fin[e] = ii < nx ? F->invm[o] : 1.0;
     fcp[e] = ii < nx ? F->cp[o] : 0.0;
@@ -439,40 +459,40 @@ __global__ void __launch_bounds__(128, 1) plane_gs_chain_smem_kernel(const Plane
   auto load = [&](int k, int sidx) {
     if (valid && k < nz) {
       const double* src = buf + P.cell0 + (long long)k * plane_cells + i + (long long)row0 * nx;
-      double* dst = stg + (size_t)sidx * ny * 64 + q + row0 * 64;
-      for (int jj = 0; jj < len; ++jj) async::cp8(dst + jj * drow * 64, src + (long long)jj * drow * nx);
+      double* dst = stg + (size_t)sidx * ny * MPC + q + row0 * MPC;
+      for (int jj = 0; jj < len; ++jj) async::cp8(dst + jj * drow * MPC, src + (long long)jj * drow * nx);
     }
     async::cp_commit();
   };
   __syncthreads();
-  for (int jj = 0; jj < len; ++jj) X[jj * 128] = 0.0;
+  for (int jj = 0; jj < len; ++jj) X[jj * T] = 0.0;
   const double* finq = fin + q;
   const double* fcpq = fcp + q;
-  const double c_own = len > 0 ? fcpq[min(len - 1, nj) * 64] : 0.0;
+  const double c_own = len > 0 ? fcpq[min(len - 1, nj) * MPC] : 0.0;
   load(0, 0);
   for (int k = 0; k < maxnz; ++k) {
     load(k + 1, (k + 1) & 1);
     async::cp_wait<1>();  // plane k (this thread's own copies) landed
-    const double* S = stg + (size_t)(k & 1) * ny * 64 + q + row0 * 64;
+    const double* S = stg + (size_t)(k & 1) * ny * MPC + q + row0 * MPC;
     const bool act = valid && k < nz;
     const double cz = k > 0 ? czw : 0.0;  // xhat(-1) = 0: X starts zeroed
     double prev = 0.0;
     if (act) {
       // rows below nj use their own factors, the rest the converged ones
       const int jn = min(len, nj);
-      const int sstep = drow * 64;
+      const int sstep = drow * MPC;
       const double* sp = S;
       double* xp = X;
       const double* fp = finq;
 #pragma unroll 4
-      for (int jj = 0; jj < jn; ++jj, sp += sstep, xp += 128, fp += 64) {
+      for (int jj = 0; jj < jn; ++jj, sp += sstep, xp += T, fp += MPC) {
         const double v = fma(-cz, *xp, *sp);
         prev = fma(-lo, prev, v) * *fp;
         *xp = prev;
       }
-      const double finf = finq[nj * 64];
+      const double finf = finq[nj * MPC];
 #pragma unroll 8
-      for (int jj = jn; jj < len; ++jj, sp += sstep, xp += 128) {
+      for (int jj = jn; jj < len; ++jj, sp += sstep, xp += T) {
         const double v = fma(-cz, *xp, *sp);
         prev = fma(-lo, prev, v) * finf;
         *xp = prev;
@@ -487,23 +507,23 @@ __global__ void __launch_bounds__(128, 1) plane_gs_chain_smem_kernel(const Plane
       double next = bot ? yB - cB * xT : xT;
       const long long dstep = (long long)drow * nx;
       double* dp = buf + P.cell0 + (long long)k * plane_cells + i + (long long)row0 * nx + (len - 1) * dstep;
-      double* xp = X + (len - 1) * 128;
+      double* xp = X + (len - 1) * T;
       *xp = next;
       *dp = next;
       int jj = len - 2;
-      const double cinf = fcpq[nj * 64];
+      const double cinf = fcpq[nj * MPC];
 #pragma unroll 8
       for (; jj >= nj; --jj) {
-        xp -= 128;
+        xp -= T;
         dp -= dstep;
         next = fma(-cinf, next, *xp);
         *xp = next;
         *dp = next;
       }
-      const double* fp = fcpq + jj * 64;
+      const double* fp = fcpq + jj * MPC;
 #pragma unroll 4
-      for (; jj >= 0; --jj, fp -= 64) {
-        xp -= 128;
+      for (; jj >= 0; --jj, fp -= MPC) {
+        xp -= T;
         dp -= dstep;
         next = fma(-*fp, next, *xp);
         *xp = next;
@@ -539,7 +559,7 @@ size_t dst_table_doubles(int nx) { return dst_geom(nx).qdoubles; }
 
 template <int KSM, int EPI, bool QSM, bool BULK, int NG>
 static cudaError_t dst_launch_t(const DstRun& R, const unsigned char* active, double omega, const double* in,
-                                double* out, int nstage, int ustaged, long long rpp, cudaStream_t s) {
+                                double* out, int nstage, int ustaged, long long rpp, int pp, cudaStream_t s) {
   const bool us = EPI != kEpiStore && ustaged;
   const DstSmem M = dst_smem(R.nx, QSM, us, nstage);
   const size_t smem = M.total(us) * sizeof(double);
@@ -554,7 +574,7 @@ static cudaError_t dst_launch_t(const DstRun& R, const unsigned char* active, do
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDstAllThreads, smem);
   const long long ntiles = (R.nrows + kDstRows - 1) / kDstRows;
   const long long grid = std::max<long long>(1, std::min<long long>(ntiles, (long long)std::max(occ, 1) * sms));
-  kern<<<(unsigned)grid, kDstAllThreads, smem, s>>>(R, active, omega, in, out, nstage, ustaged, rpp);
+  kern<<<(unsigned)grid, kDstAllThreads, smem, s>>>(R, active, omega, in, out, nstage, ustaged, rpp, pp);
   return cudaGetLastError();
 }
 
@@ -566,23 +586,34 @@ static cudaError_t dst_launch_k(const DstRun& R, const unsigned char* active, do
   const size_t cap = 227 * 1024 - 2048;  // opt-in limit less the static shared memory
   // preference: split table on chip, three then two input stages, staged u
   // rows; dropped in the reverse order until the layout fits
+  // Layout preference.  Store epilogue: split table on chip, three stages
+  // (two ping-pong consumer groups plus one stage loading).  Relax
+  // epilogues also stage the u rows (their direct loads are latency-bound):
+  // table on chip, two stages, one consumer group (measured at C4: 1.14 ms,
+  // against 1.29 with two groups on two stages and 2.15 with the table read
+  // through L1/L2 to make room for three stages).
   bool qsm = true;
-  int nstage = kDstStages, ustaged = relax ? 1 : 0;
+  int nstage = kDstStages, ustaged = relax ? 1 : 0, pp = 1;
+  if (relax) {
+    nstage = 2;
+    pp = 0;
+  }
   auto fits = [&] { return dst_smem(R.nx, qsm, ustaged, nstage).total(ustaged) * 8 <= cap; };
   if (!fits()) nstage = 2;
   if (!fits()) qsm = false;
   if (!fits()) nstage = kDstStages;
   if (!fits()) nstage = 2;
   if (!fits()) ustaged = 0;
-  if (!fits()) return cudaErrorInvalidValue;  // the two consumer groups need two stages
+  if (!fits()) nstage = 1;
+  if (!fits()) return cudaErrorInvalidValue;
   // bulk copies need 16-byte aligned rows: even nx and an even workspace offset
   const bool bulk = (R.nx % 2 == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
   // eight independent DMMA accumulator chains per warp when the n-tiles
   // come in eights, else four
   const bool ng8 = G.nt % 8 == 0;
 #define PSM_DST_NG(K_, Q_, B_) \
-  return ng8 ? dst_launch_t<K_, EPI, Q_, B_, 8>(R, active, omega, in, out, nstage, ustaged, rpp, s) \
-             : dst_launch_t<K_, EPI, Q_, B_, 4>(R, active, omega, in, out, nstage, ustaged, rpp, s)
+  return ng8 ? dst_launch_t<K_, EPI, Q_, B_, 8>(R, active, omega, in, out, nstage, ustaged, rpp, pp, s) \
+             : dst_launch_t<K_, EPI, Q_, B_, 4>(R, active, omega, in, out, nstage, ustaged, rpp, pp, s)
 #define PSM_DST(K_)                        \
   if (qsm) {                               \
     if (bulk) PSM_DST_NG(K_, true, true);  \
@@ -613,15 +644,20 @@ cudaError_t launch_dst_rows(int epi, const PatchDev* patches, int p0, int p1, lo
   return cudaErrorInvalidValue;
 }
 
+template <int MPC>
+static size_t chain_smem_bytes(int ny, int nj) {
+  return (2 * (size_t)ny * MPC + (size_t)(ny - ny / 2) * 2 * MPC + 2 * (size_t)(nj + 1) * MPC) * sizeof(double);
+}
+
+template <int MPC>
 static cudaError_t chain_smem_launch(const PlaneFac* d_fac, int nx, int ny, const PatchDev* patches, int p0, int np,
                                     int maxnz, double czw, double* buf, int nj, cudaStream_t s) {
-  const int cpp = (nx + 63) / 64;
-  const size_t smem = (2 * (size_t)ny * 64 + (size_t)(ny - ny / 2) * 128 + 2 * (size_t)(nj + 1) * 64) * sizeof(double);
-  if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e =
-      cudaFuncSetAttribute(plane_gs_chain_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int cpp = (nx + MPC - 1) / MPC;
+  const size_t smem = chain_smem_bytes<MPC>(ny, nj);
+  auto kern = plane_gs_chain_smem_kernel<MPC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  plane_gs_chain_smem_kernel<<<(unsigned)(np * cpp), 128, smem, s>>>(d_fac, patches, p0, cpp, maxnz, czw, buf, nj);
+  kern<<<(unsigned)(np * cpp), 2 * MPC, smem, s>>>(d_fac, patches, p0, cpp, maxnz, czw, buf, nj);
   return cudaGetLastError();
 }
 
@@ -631,10 +667,16 @@ cudaError_t launch_plane_gs_chain(const PlaneFac* d_fac, int nx, int ny, int nj,
                                   int np, int maxnz, double czw, double* buf, cudaStream_t s) {
   const long long nlines = (long long)np * nx;
   if (nlines == 0) return cudaSuccess;
-  // on-chip chains while their working set fits one SM (ny <= 128 at nj <= 48)
-  const size_t smem = (2 * (size_t)ny * 64 + (size_t)(ny - ny / 2) * 128 + 2 * (size_t)(nj + 1) * 64) * sizeof(double);
-  if (nj >= 0 && smem <= 220 * 1024 && !getenv("PSM_PLANE_CHAIN_GLOBAL"))
-    return chain_smem_launch(d_fac, nx, ny, patches, p0, np, maxnz, czw, buf, nj, s);
+  // on-chip chains while their working set fits one SM: 32 modes per CTA
+  // (two CTAs per SM at ny = 128), 64 when more CTAs would not fit anyway
+  if (nj >= 0 && !getenv("PSM_PLANE_CHAIN_GLOBAL")) {
+    const char* e = getenv("PSM_PLANE_CHAIN_MPC");
+    const int mpc = e ? atoi(e) : 32;
+    if (mpc == 32 && chain_smem_bytes<32>(ny, nj) <= 110 * 1024)
+      return chain_smem_launch<32>(d_fac, nx, ny, patches, p0, np, maxnz, czw, buf, nj, s);
+    if (chain_smem_bytes<64>(ny, nj) <= 220 * 1024)
+      return chain_smem_launch<64>(d_fac, nx, ny, patches, p0, np, maxnz, czw, buf, nj, s);
+  }
   plane_gs_chain_kernel<<<(unsigned)((2 * nlines + 127) / 128), 128, 0, s>>>(d_fac, patches, p0, nlines, maxnz, czw,
                                                                              buf);
   return cudaGetLastError();
