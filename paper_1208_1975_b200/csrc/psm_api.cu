@@ -94,7 +94,8 @@ namespace psm {
 cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                              double omega, const int4* blocks, int nblocks, int inplace, int mx, int my, int mz,
                              int bx, int by, int bz, cudaStream_t s, const int4* gsdep = nullptr,
-                             int* flags = nullptr, int* ticket = nullptr);
+                             int* flags = nullptr, int* ticket = nullptr, const void* tmaps = nullptr);
+cudaError_t box_build_tmaps(const PatchDev* hp, int npatch, void** out);
 cudaError_t launch_box_apply(const BoxFac* F, const double* r, double* x, long long count, cudaStream_t s);
 }
 extern int psm_plane_band_mode;  // psm_plane.cu
@@ -496,6 +497,7 @@ int psm_plan_create(const psm_patch_desc* patches, int npatch, const psm_copy_de
     if (e == cudaSuccess) e = cudaMalloc(&P->d_box_regions, std::max<size_t>(16, regs.size() * sizeof(int)));
     if (e == cudaSuccess)
       e = cudaMemcpy(P->d_box_regions, regs.data(), regs.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = box_build_tmaps(P->hp.data(), npatch, &P->d_box_tmaps);
     if (e != cudaSuccess) {
       psm_plan_destroy(P);
       return fail(PSM_ECUDA, "box block list: %s", cudaGetErrorString(e));
@@ -530,6 +532,7 @@ int psm_plan_destroy(psm_plan* P) {
   cudaFree(P->d_box_regions);
   cudaFree(P->d_box_deps);
   cudaFree(P->d_box_flags);
+  cudaFree(P->d_box_tmaps);
   psm_gs_pipe_free(P);
   for (auto& kv : P->unit_cache) cudaFree(kv.second.first);
   for (auto& kv : P->active_cache) cudaFree(kv.second);
@@ -883,7 +886,8 @@ int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int
       P->launches += 1;
     }
     CUDA_TRY(launch_box_sweep(P->d_patches, da, P->st, omega, P->d_box_regions, P->nregions, 0, P->reg_m[0],
-                              P->reg_m[1], P->reg_m[2], P->box_dims[0], P->box_dims[1], P->box_dims[2], s));
+                              P->reg_m[1], P->reg_m[2], P->box_dims[0], P->box_dims[1], P->box_dims[2], s, nullptr,
+                              nullptr, nullptr, P->d_box_tmaps));
     P->launches += 1;
     return PSM_OK;
   }
@@ -1297,7 +1301,7 @@ int psm_gs_sweep(psm_plan* P, const unsigned char* active, double omega, int mod
     if (tmpl && !(env && env[0] == '1')) {
       CUDA_TRY(cudaMemsetAsync(P->d_box_flags, 0, (size_t)(P->nboxes + 1) * sizeof(int), s));
       CUDA_TRY(launch_box_sweep(P->d_patches, da, P->st, omega, P->d_boxes, P->nboxes, 1, 1, 1, 1, bx, by, bz, s,
-                                P->d_box_deps, P->d_box_flags, P->d_box_flags + P->nboxes));
+                                P->d_box_deps, P->d_box_flags, P->d_box_flags + P->nboxes, P->d_box_tmaps));
       P->launches += 1;
       return PSM_OK;
     }

@@ -42,6 +42,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(sa(b))
       : "memory");
 }
+// 3-D tiled tensor copy (TMA) of the box at element coordinates (x, y, z) of
+// the tensor map into dense shared memory (128-byte aligned); out-of-range
+// elements are zero-filled and still count towards the transaction bytes
+__device__ __forceinline__ void tensor3d_g2s(void* dst, const void* tmap, int x, int y, int z, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(sa(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(sa(b))
+      : "memory");
+}
 __device__ __forceinline__ void cp8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa(dst)), "l"(src) : "memory");
 }

@@ -35,9 +35,12 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <vector>
 
+#include "psm_async.cuh"
 #include "psm_internal.cuh"
 
 namespace psm {
@@ -46,6 +49,14 @@ constexpr int kBoxMax = 8;     // largest extent per axis
 constexpr int kBoxT = 128;     // threads per block CTA
 constexpr int kHs = 10;        // halo box row stride (ex + 2 <= 10)
 constexpr int kHp = 100;       // halo box plane stride
+constexpr int kHslot = 1008;   // halo staging slot (kHp * 10 rounded to 128 bytes, for TMA)
+constexpr int kTmapBytes = 128;  // sizeof(CUtensorMap)
+#ifndef PSM_BOX_MINB
+// resident CTAs per SM the sweep kernel is register-limited to (6: 80
+// registers; holding the DMMA A fragments in registers instead of shared
+// memory needs 5 and measured 13% slower on F1)
+#define PSM_BOX_MINB 6
+#endif
 #ifndef PSM_BOX_RS
 #define PSM_BOX_RS 12
 #define PSM_BOX_RP 100
@@ -197,10 +208,6 @@ __global__ void __launch_bounds__(kBoxT) box_sweep_kernel(const PatchDev* __rest
 // the 8x8 block-diagonal composition of the block transform (blockdiag of
 // 8/B copies of the B x B matrix), X the 8 x 64 line matrix.  4 warps x 2
 // line tiles x 2 k-steps: 16 DMMA per pass instead of 4,096 scalar FMAs.
-__device__ __forceinline__ int box_addr(int axis, int n, int p) {
-  return axis == 0 ? (n >> 3) * kRp + (n & 7) * kRs + p
-                   : axis == 1 ? (n >> 3) * kRp + p * kRs + (n & 7) : p * kRp + (n >> 3) * kRs + (n & 7);
-}
 __device__ __forceinline__ void box_dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
@@ -215,27 +222,6 @@ __device__ __forceinline__ void box_afrag(const double* __restrict__ T, int lane
     a[ks] = (r / BS == c / BS) ? __ldg(T + (r % BS) * 8 + (c % BS)) : 0.0;
   }
 }
-template <int BX, int BY, int BZ>
-__device__ __forceinline__ void box_pass_mma(double* wc, int axis, const double (&a)[2], int lane, int warp,
-                                             const double* sc /* 4 per lane or null */) {
-#pragma unroll
-  for (int tt = 0; tt < 2; ++tt) {
-    const int t = warp * 2 + tt;
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks)
-      box_dmma(d0, d1, a[ks], wc[box_addr(axis, 8 * t + (lane >> 2), 4 * ks + (lane & 3))]);
-    const int p = lane >> 2, n0 = 8 * t + 2 * (lane & 3);
-    if (sc) {  // forward z pass: scale by 1/lambda (p = k, line n = (i, j))
-      d0 *= sc[2 * tt];
-      d1 *= sc[2 * tt + 1];
-    }
-    __syncwarp();
-    wc[box_addr(axis, n0, p)] = d0;
-    wc[box_addr(axis, n0 + 1, p)] = d1;
-  }
-}
-
 // The same sweep with compile-time block dims and region multipliers: a
 // fixed thread-to-cell/line mapping replaces the runtime integer divisions
 // that dominated the generic kernel's instruction count (ncu: 28% IMAD plus
@@ -253,22 +239,75 @@ __device__ __forceinline__ int box_ld_relaxed(const int* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Interior 8^3 regions run the six transforms as DMMA m8n8k4 passes with the
+// data in fragment registers: lane (r = lane/4, c = lane%4) of warp w holds,
+// per tile tt (plane 2w+tt), the B operand X[4ks+c][r] and the result D[r][2c+e].
+// Only the two axis changes that cross warps (y -> z, z -> y) go through the
+// work cube; x -> y, z -> z' and y' -> x' are register shuffles.  The line
+// orders below make every shared-memory access conflict-free (two wavefronts
+// per 8-byte warp access; tools/box_lanes_sim.py checks the orders, the
+// conflicts and the arithmetic):
+//   x pass    line r -> row j = box_jx(r)       (residual loads from the halo)
+//   y pass    line r -> column i = box_ip(r)    (results stored to the cube)
+//   z, z'     line r -> i = r, i = box_ip(r)    (z' results stored to the cube)
+//   y', x'    line r -> i = r, j = r            (x' results relaxed from registers)
+__device__ __forceinline__ int box_jx(int n) { return 2 * (n & 3) + (n >> 2); }
+__device__ __forceinline__ int box_ip(int n) { return (n >> 1) + 4 * (n & 1); }
+__device__ __forceinline__ void box_mma2(const double (&a)[2], const double (&bq)[2], double (&d)[2]) {
+  d[0] = 0.0;
+  d[1] = 0.0;
+  box_dmma(d[0], d[1], a[0], bq[0]);
+  box_dmma(d[0], d[1], a[1], bq[1]);
+}
+// (e ? v1 : v0) of lane src
+__device__ __forceinline__ double box_shfl_pick(const double (&d)[2], int src, int e) {
+  const double v0 = __shfl_sync(0xffffffffu, d[0], src), v1 = __shfl_sync(0xffffffffu, d[1], src);
+  return e ? v1 : v0;
+}
+
 template <int BX, int BY, int BZ, int MX, int MY, int MZ>
-__global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restrict__ patches,
+__global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDev* __restrict__ patches,
                                                      const unsigned char* __restrict__ active, StencilDev st,
                                                      double omega, const int4* __restrict__ blocks, int nblocks,
                                                      int inplace, const int4* __restrict__ gsdep, int* flags,
-                                                     int* ticket) {
+                                                     int* ticket, const char* __restrict__ tmaps) {
   constexpr int RX = BX * MX, RY = BY * MY, RZ = BZ * MZ;
   constexpr int HX = RX + 2, HY = RY + 2, HN = HX * HY * (RZ + 2);
   constexpr int NC = RX * RY * RZ;
-  // double-buffered staging: the next region's u halo and f stream in with
-  // cp.async while this region computes (the sweep is otherwise latency-bound)
-  __shared__ __align__(16) double hbuf[2][kHp * kHs];
-  __shared__ __align__(16) double fbuf[2][NC];
+  // 8^3 regions: the halo box is staged dense (10^3: row stride kHs, plane
+  // stride kHp) and f with row stride 10 (conflict-free fragment loads), so
+  // two TMA tensor copies (one thread) replace ~760 cp.async requests
+  constexpr bool kShape8 = RX == 8 && RY == 8 && RZ == 8;
+  constexpr int FS = kShape8 ? 10 : RX;  // f staging row stride
+  constexpr int FN = FS * RY * RZ;
+  const bool tma = kShape8 && tmaps != nullptr;
+  // double-buffered staging: the next region's u halo and f stream in
+  // while this region computes (the sweep is otherwise latency-bound)
+  __shared__ __align__(128) double hbuf[2][kHslot];
+  __shared__ __align__(128) double fbuf[2][FN];
   __shared__ double wc[kBoxMax * kRp];
+  __shared__ uint64_t tbar[2];
   const int tid = threadIdx.x;
+  uint32_t tphase = 0;  // parity of each slot's next TMA completion
+  if (tma) {
+    if (tid == 0) {
+      async::bar_init(&tbar[0], 1);
+      async::bar_init(&tbar[1], 1);
+      async::bar_fence_init();
+    }
+    __syncthreads();
+  }
   auto stage = [&](int b, int slot) {
+    if (tma) {
+      if (tid == 0 && b < nblocks) {
+        const int4 B = blocks[b];
+        const char* m = tmaps + (size_t)(3 * B.x) * kTmapBytes;
+        async::bar_expect(&tbar[slot], (uint32_t)((kHp * kHs + FN) * sizeof(double)));
+        async::tensor3d_g2s(&hbuf[slot][0], m + active[B.x] * kTmapBytes, B.y, B.z, B.w, &tbar[slot]);
+        async::tensor3d_g2s(&fbuf[slot][0], m + 2 * kTmapBytes, B.y, B.z, B.w, &tbar[slot]);
+      }
+      return;
+    }
     if (b < nblocks) {
       const int4 B = blocks[b];
       const PatchDev& P = patches[B.x];
@@ -292,7 +331,7 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
         for (int q = tid; q < FW * RY * RZ; q += kBoxT) {
           const int k = q / (FW * RY), r = q - k * (FW * RY), j = r / FW, a = r - j * FW;
           if (j < ry && k < rz)
-            box_cp16(&fbuf[slot][(k * RY + j) * RX + 2 * a], fb0 + ((long long)k * ny + j) * nx + 2 * a);
+            box_cp16(&fbuf[slot][(k * RY + j) * FS + 2 * a], fb0 + ((long long)k * ny + j) * nx + 2 * a);
         }
       } else {
         for (int q = tid; q < HN; q += kBoxT) {
@@ -303,45 +342,92 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
         for (int q = tid; q < NC; q += kBoxT) {
           const int k = q / (RX * RY), r = q - k * (RX * RY), j = r / RX, i = r - j * RX;
           if (i < rx && j < ry && k < rz)
-            box_cp8(&fbuf[slot][q], fb0 + ((long long)k * ny + j) * nx + i);
+            box_cp8(&fbuf[slot][(k * RY + j) * FS + i], fb0 + ((long long)k * ny + j) * nx + i);
         }
       }
     }
     box_commit();
   };
-  __shared__ int gs_b;
+  __shared__ int gs_b, gs_nxt[2];
   const bool gsp = gsdep != nullptr;
+  // GS with TMA staging: each CTA holds two tickets, the block it computes
+  // and the next one, whose halo is prefetched into the other slot as soon
+  // as its predecessors are done (polled once while the current block
+  // computes, waited for only after the current block is released, so no
+  // CTA ever waits while holding an unreleased block)
+  const bool gpre = gsp && tma;
+  auto gs_ready = [&](int tk, bool block) {
+    const int4 d = gsdep[tk];
+    const int pred[3] = {d.y, d.z, d.w};
+    for (int q = 0; q < 3; ++q)
+      if (pred[q] >= 0) {
+        if (!block && box_ld_relaxed(flags + pred[q]) == 0) return false;
+        while (box_ld_relaxed(flags + pred[q]) == 0) {
+        }
+      }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // the TMA reads of the halo go through the async proxy
+    if (tma) asm volatile("fence.proxy.async.global;" ::: "memory");
+    return true;
+  };
   if (!gsp) stage(blockIdx.x, 0);
-  int slot = 0;
-  const BoxFac* afF = nullptr;  // factor object whose fragments af/scl hold
-  double af[6][2], scl[4];
+  int slot = 0, gcur = 0;
+  if (gpre) {
+    if (tid == 0) {
+      const int tk = atomicAdd(ticket, 1);
+      if (tk < nblocks) {
+        gs_ready(tk, true);
+        stage(tk, 0);
+      }
+      gs_b = tk;
+    }
+    __syncthreads();
+    gcur = gs_b;
+  }
+  const BoxFac* afF = nullptr;  // factor object whose fragments afs/scl hold
+  double scl[2][2];
+  __shared__ double afs[6][2][32];  // A fragments of the six transforms (lane-indexed)
+  const int lane = tid & 31, warp = tid >> 5, lr = lane >> 2, lc = lane & 3;
   for (int b = blockIdx.x;; b += gridDim.x, slot ^= 1) {
-    if (gsp) {
+    if (gpre) {
+      b = gcur;
+      if (b >= nblocks) break;
+      async::bar_wait(&tbar[slot], (tphase >> slot) & 1);
+      tphase ^= 1u << slot;
+      if (tid == 0) {  // next ticket; prefetch now if its predecessors are done
+        const int nt = atomicAdd(ticket, 1);
+        const bool now = nt < nblocks && gs_ready(nt, false);
+        if (now) stage(nt, slot ^ 1);
+        gs_nxt[slot] = now ? nt : -2 - nt;
+      }
+    } else if (gsp) {
       slot = 0;
       if (tid == 0) {
         const int tk = atomicAdd(ticket, 1);
-        if (tk < nblocks) {
-          const int4 d = gsdep[tk];
-          const int pred[3] = {d.y, d.z, d.w};
-          for (int q = 0; q < 3; ++q)
-            if (pred[q] >= 0)
-              while (box_ld_relaxed(flags + pred[q]) == 0) {
-              }
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        }
+        if (tk < nblocks) gs_ready(tk, true);
         gs_b = tk;
       }
       __syncthreads();
       b = gs_b;
       if (b >= nblocks) break;
       stage(b, 0);
-      box_wait<0>();
+      if (tma) {
+        async::bar_wait(&tbar[0], tphase & 1);
+        tphase ^= 1;
+      } else {
+        box_wait<0>();
+      }
       __syncthreads();
     } else {
       if (b >= nblocks) break;
-      stage(b + gridDim.x, slot ^ 1);
-      box_wait<1>();
-      __syncthreads();
+      if (!tma) stage(b + gridDim.x, slot ^ 1);  // (TMA: issued after the first barrier below)
+      if (tma) {
+        async::bar_wait(&tbar[slot], (tphase >> slot) & 1);
+        tphase ^= 1u << slot;
+      } else {
+        box_wait<1>();
+        __syncthreads();
+      }
     }
     const double* hb = hbuf[slot];
     const double* fb = fbuf[slot];
@@ -354,64 +440,154 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
     const long long px = nx + 2, pxy = px * (ny + 2);
     const int act = active[B.x];
     double* __restrict__ v = P.buf[inplace ? act : act ^ 1];
-#pragma unroll
-    for (int q0 = 0; q0 < NC; q0 += kBoxT) {
-      const int q = q0 + tid;
-      const int k = q / (RX * RY), r = q - k * (RX * RY), j = r / RX, i = r - j * RX;
-      if (q < NC && i < rx && j < ry && k < rz) {
-        const int h = (k + 1) * kHp + (j + 1) * kHs + i + 1;
-        wc[k * kRp + j * kRs + i] = residual7(st, fb[q], hb[h], hb[h - 1], hb[h + 1], hb[h - kHs], hb[h + kHs],
-                                              hb[h - kHp], hb[h + kHp]);
+    bool interior8 = false;
+    if constexpr (MX * BX == 8 && MY * BY == 8 && MZ * BZ == 8) interior8 = rx == 8 && ry == 8 && rz == 8;
+    if (!interior8) {
+      // edge region (or a TMA-less launch still holding the other slot's copy):
+      // the prefetch of the next region cannot wait for the first barrier
+      // (an interior region before this one ends without a barrier)
+      if (tma && !gsp) {
+        __syncthreads();
+        stage(b + gridDim.x, slot ^ 1);
       }
+#pragma unroll
+      for (int q0 = 0; q0 < NC; q0 += kBoxT) {
+        const int q = q0 + tid;
+        const int k = q / (RX * RY), r = q - k * (RX * RY), j = r / RX, i = r - j * RX;
+        if (q < NC && i < rx && j < ry && k < rz) {
+          const int h = (k + 1) * kHp + (j + 1) * kHs + i + 1;
+          wc[k * kRp + j * kRs + i] = residual7(st, fb[(k * RY + j) * FS + i], hb[h], hb[h - 1], hb[h + 1],
+                                                hb[h - kHs], hb[h + kHs], hb[h - kHp], hb[h + kHp]);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    bool done = false;
     if constexpr (MX * BX == 8 && MY * BY == 8 && MZ * BZ == 8) {
-      if (rx == 8 && ry == 8 && rz == 8) {  // interior region: tensor-core passes
-        const int lane = tid & 31, warp = tid >> 5;
+      if (interior8) {
         if (F != afF) {  // A fragments of the six transforms and this lane's 1/lambda, per factor object
           afF = F;
-          box_afrag<BX>(box_mat(F->F, 0, BX), lane, af[0]);
-          box_afrag<BY>(box_mat(F->F, 1, BY), lane, af[1]);
-          box_afrag<BZ>(box_mat(F->F, 2, BZ), lane, af[2]);
-          box_afrag<BZ>(box_mat(F->B, 2, BZ), lane, af[3]);
-          box_afrag<BY>(box_mat(F->B, 1, BY), lane, af[4]);
-          box_afrag<BX>(box_mat(F->B, 0, BX), lane, af[5]);
+          if (warp == 0) {
+            double a[2];
+            box_afrag<BX>(box_mat(F->F, 0, BX), lane, a);
+            afs[0][0][lane] = a[0], afs[0][1][lane] = a[1];
+            box_afrag<BY>(box_mat(F->F, 1, BY), lane, a);
+            afs[1][0][lane] = a[0], afs[1][1][lane] = a[1];
+            box_afrag<BZ>(box_mat(F->F, 2, BZ), lane, a);
+            afs[2][0][lane] = a[0], afs[2][1][lane] = a[1];
+            box_afrag<BZ>(box_mat(F->B, 2, BZ), lane, a);
+            afs[3][0][lane] = a[0], afs[3][1][lane] = a[1];
+            box_afrag<BY>(box_mat(F->B, 1, BY), lane, a);
+            afs[4][0][lane] = a[0], afs[4][1][lane] = a[1];
+            box_afrag<BX>(box_mat(F->B, 0, BX), lane, a);
+            afs[5][0][lane] = a[0], afs[5][1][lane] = a[1];
+          }
+          // z-pass result (k = lr, i = 2 lc + e) of the plane j = 2 warp + tt
 #pragma unroll
-          for (int tt = 0; tt < 2; ++tt) {
-            const int n0 = 8 * (warp * 2 + tt) + 2 * (lane & 3), pz = lane >> 2;
+          for (int tt = 0; tt < 2; ++tt)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
-              scl[2 * tt + e] = box_ilam(F->IL, BX, BY, BZ, ((n0 + e) & 7) % BX, ((n0 + e) >> 3) % BY, pz % BZ);
-          }
+              scl[tt][e] = box_ilam(F->IL, BX, BY, BZ, (2 * lc + e) % BX, (2 * warp + tt) % BY, lr % BZ);
+          __syncthreads();  // afs (F is uniform over the CTA)
         }
-        box_pass_mma<BX, BY, BZ>(wc, 0, af[0], lane, warp, nullptr);
-        __syncthreads();
-        box_pass_mma<BX, BY, BZ>(wc, 1, af[1], lane, warp, nullptr);
-        __syncthreads();
-        box_pass_mma<BX, BY, BZ>(wc, 2, af[2], lane, warp, scl);
-        __syncthreads();
-        box_pass_mma<BX, BY, BZ>(wc, 2, af[3], lane, warp, nullptr);
-        __syncthreads();
-        box_pass_mma<BX, BY, BZ>(wc, 1, af[4], lane, warp, nullptr);
-        __syncthreads();
-        box_pass_mma<BX, BY, BZ>(wc, 0, af[5], lane, warp, nullptr);
-        __syncthreads();
+        double bq[2][2], d[2][2];
+#define PSM_BOX_A(P) const double A##P[2] = {afs[P][0][lane], afs[P][1][lane]};
+        // residual (reference operation order) straight into the x-pass B
+        // fragments: cells (i = 4 ks + lc, j = box_jx(lr), k = 2 warp + tt)
+        // (the two planes of a lane are each other's z neighbours)
+        const int jr = box_jx(lr);
 #pragma unroll
-        for (int q0 = 0; q0 < 512; q0 += kBoxT) {  // relax, row-contiguous stores
-          const int q = q0 + tid, k = q >> 6, j = (q >> 3) & 7, i = q & 7;
-          const double nv = relax(hb[(k + 1) * kHp + (j + 1) * kHs + i + 1], omega, wc[k * kRp + j * kRs + i]);
-          double* vp = v + (long long)(z0 + k + 1) * pxy + (long long)(y0 + j + 1) * px + x0 + i + 1;
-          *vp = nv;
-          if (!inplace) {
-            if (x0 + i == 0) vp[-1] = -nv;
-            if (x0 + i == nx - 1) vp[1] = -nv;
+        for (int ks = 0; ks < 2; ++ks) {
+          const int k = 2 * warp, i = 4 * ks + lc;
+          const int h = (k + 1) * kHp + (jr + 1) * kHs + i + 1, h1 = h + kHp;
+          const double c0 = hb[h], c1 = hb[h1];
+          bq[0][ks] = residual7(st, fb[(k * 8 + jr) * FS + i], c0, hb[h - 1], hb[h + 1], hb[h - kHs], hb[h + kHs],
+                                hb[h - kHp], c1);
+          bq[1][ks] = residual7(st, fb[((k + 1) * 8 + jr) * FS + i], c1, hb[h1 - 1], hb[h1 + 1], hb[h1 - kHs],
+                                hb[h1 + kHs], c0, hb[h1 + kHp]);
+        }
+        // x pass; x -> y by shuffle: lane needs (i = box_ip(lr), j = 4 ks + lc)
+PSM_BOX_A(0)
+        #pragma unroll
+        for (int tt = 0; tt < 2; ++tt) box_mma2(A0, bq[tt], d[tt]);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int ns = 2 * ks + (lc >> 1) + 4 * (lc & 1);  // x-pass line of row j = 4 ks + lc
+            bq[tt][ks] = box_shfl_pick(d[tt], box_ip(lr) * 4 + (ns >> 1), ns & 1);
+          }
+        // y pass -> cube (k = 2 warp + tt, j = lr, i = box_ip(2 lc + e))
+PSM_BOX_A(1)
+        #pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          box_mma2(A1, bq[tt], d[tt]);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) wc[(2 * warp + tt) * kRp + lr * kRs + box_ip(2 * lc + e)] = d[tt][e];
+        }
+        __syncthreads();
+        // every warp is past this region's halo reads of the previous slot:
+        // prefetch the next region into it
+        if (tma && !gsp) stage(b + gridDim.x, slot ^ 1);
+        // z pass (plane j = 2 warp + tt, line i = lr), scaled by 1/lambda;
+        // z -> z' by shuffle: lane needs (k = 4 ks + lc, i = box_ip(lr))
+PSM_BOX_A(2)
+        #pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = wc[(4 * ks + lc) * kRp + (2 * warp + tt) * kRs + lr];
+          box_mma2(A2, bq[tt], d[tt]);
+          d[tt][0] *= scl[tt][0];
+          d[tt][1] *= scl[tt][1];
+        }
+        const int ir = box_ip(lr);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = box_shfl_pick(d[tt], (4 * ks + lc) * 4 + (ir >> 1), ir & 1);
+        // z' pass -> cube (k = lr, j = 2 warp + tt, i = box_ip(2 lc + e))
+PSM_BOX_A(3)
+        #pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          box_mma2(A3, bq[tt], d[tt]);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) wc[lr * kRp + (2 * warp + tt) * kRs + box_ip(2 * lc + e)] = d[tt][e];
+        }
+        __syncthreads();
+        // y' pass (plane k = 2 warp + tt, line i = lr); y' -> x' by shuffle:
+        // lane needs (j = lr, i = 4 ks + lc)
+PSM_BOX_A(4)
+        #pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = wc[(2 * warp + tt) * kRp + (4 * ks + lc) * kRs + lr];
+          box_mma2(A4, bq[tt], d[tt]);
+        }
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = box_shfl_pick(d[tt], lr * 4 + ((4 * ks + lc) >> 1), lc & 1);
+        // x' pass: result (i = lr, j = 2 lc + e, k = 2 warp + tt); relax and store
+PSM_BOX_A(5)
+        #pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          box_mma2(A5, bq[tt], d[tt]);
+          const int k = 2 * warp + tt;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 2 * lc + e;
+            const double nv = relax(hb[(k + 1) * kHp + (j + 1) * kHs + lr + 1], omega, d[tt][e]);
+            double* vp = v + (long long)(z0 + k + 1) * pxy + (long long)(y0 + j + 1) * px + x0 + lr + 1;
+            *vp = nv;
+            if (!inplace) {
+              if (x0 + lr == 0) vp[-1] = -nv;
+              if (x0 + lr == nx - 1) vp[1] = -nv;
+            }
           }
         }
-        done = true;
+#undef PSM_BOX_A
       }
     }
-    if (!done) {
+    if (!interior8) {
       // forward x: lines (q, j, k)
   #pragma unroll
       for (int l0 = 0; l0 < MX * RY * RZ; l0 += kBoxT) {
@@ -474,7 +650,7 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
           double* vrow = v + (long long)(z0 + k + 1) * pxy + (long long)(y0 + j + 1) * px + x0 + i0 + 1;
           const double* hrow = hb + (k + 1) * kHp + (j + 1) * kHs + i0 + 1;
   #pragma unroll
-          for (int i = 0; i < BX; ++i) {  // (hb of this slot is not restaged before the loop-top barrier)
+          for (int i = 0; i < BX; ++i) {  // (hb of this slot is not restaged before the loop-end barrier)
             if (i < ex) {
               const double nv = relax(hrow[i], omega, w[i]);
               vrow[i] = nv;
@@ -487,10 +663,21 @@ __global__ void __launch_bounds__(kBoxT, 5) box_sweep_t(const PatchDev* __restri
         }
       }
     }
-    __syncthreads();
+    // the interior path needs no barrier here: its cube accesses after the
+    // second barrier are warp-local and the next prefetch waited for the
+    // first; edge regions, the cp.async staging and the GS release do
+    if (!interior8 || !tma || gsp) __syncthreads();
     if (gsp && tid == 0) {  // every thread's stores precede the barrier above: release them
       __threadfence();
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + gsdep[b].x), "r"(1) : "memory");
+    }
+    if (gpre) {
+      const int code = gs_nxt[slot];
+      gcur = code >= 0 ? code : -2 - code;
+      if (code < 0 && tid == 0 && gcur < nblocks) {  // not prefetched: wait now (this block is released)
+        gs_ready(gcur, true);
+        stage(gcur, slot ^ 1);
+      }
     }
   }
 }
@@ -533,28 +720,85 @@ __global__ void __launch_bounds__(kBoxT) box_apply_kernel(const BoxFac* __restri
   }
 }
 
+// Tensor maps for the TMA staging of 8^3 regions, 3 per patch: buf[0] and
+// buf[1] (padded (nx+2, ny+2, nz+2), box 10^3) and f ((nx, ny, nz), box
+// 10 x 8 x 8: rows padded to the staging stride FS).  Needs 16-byte aligned bases and strides (nx even); *out stays null
+// (cp.async staging) otherwise, or with PSM_BOX_TMA=0.
+typedef CUresult (*EncodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+cudaError_t box_build_tmaps(const PatchDev* hp, int npatch, void** out) {
+  *out = nullptr;
+  const char* env = getenv("PSM_BOX_TMA");
+  if (env && env[0] == '0') return cudaSuccess;
+  static EncodeTiled_t encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (EncodeTiled_t)fn;
+  }();
+  if (!encode || npatch <= 0) return cudaSuccess;
+  static_assert(sizeof(CUtensorMap) == kTmapBytes, "tensor map size");
+  std::vector<CUtensorMap> maps(3 * (size_t)npatch);
+  for (int p = 0; p < npatch; ++p) {
+    const PatchDev& h = hp[p];
+    if ((h.nx & 1) || (((uintptr_t)h.buf[0] | (uintptr_t)h.buf[1] | (uintptr_t)h.f) & 15)) return cudaSuccess;
+    for (int k = 0; k < 3; ++k) {
+      const bool fmap = k == 2;
+      const cuuint64_t dims[3] = {(cuuint64_t)h.nx + (fmap ? 0 : 2), (cuuint64_t)h.ny + (fmap ? 0 : 2),
+                                  (cuuint64_t)h.nz + (fmap ? 0 : 2)};
+      const cuuint64_t strides[2] = {dims[0] * 8, dims[0] * dims[1] * 8};
+      const cuuint32_t box[3] = {10u, fmap ? 8u : 10u, fmap ? 8u : 10u};  // f rows padded to 10 (FS)
+      const cuuint32_t estr[3] = {1, 1, 1};
+      void* base = fmap ? (void*)h.f : (void*)h.buf[k];
+      if (encode(&maps[3 * p + k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaSuccess;
+    }
+  }
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, maps.size() * sizeof(CUtensorMap));
+  if (e == cudaSuccess) e = cudaMemcpy(d, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return e;
+  }
+  *out = d;
+  return cudaSuccess;
+}
+
 // bx, by, bz: the launch's common block dims (0 if the blocks differ);
 // shapes of the reference's DEFAULT_BLOCK_SIZES get the compile-time kernel.
 cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* active, const StencilDev& st,
                              double omega, const int4* blocks, int nblocks, int inplace, int mx, int my, int mz,
-                             int bx, int by, int bz, cudaStream_t s, const int4* gsdep, int* flags, int* ticket) {
+                             int bx, int by, int bz, cudaStream_t s, const int4* gsdep, int* flags, int* ticket,
+                             const void* tmaps) {
   if (nblocks <= 0) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(nblocks, 16 * sms);
+  const int grid = std::min(nblocks, 16 * sms);  // persistent over the region list
   const bool region = mx * bx == 8 && my * by == 8 && mz * bz == 8;  // Jacobi regions of 8^3
   const bool single = mx == 1 && my == 1 && mz == 1;
+  const char* tm = (const char*)tmaps;
 #define PSM_BOXT(X, Y, Z)                                                                                      \
   if (bx == X && by == Y && bz == Z) {                                                                        \
     if (region) {                                                                                             \
+      cudaFuncSetAttribute(box_sweep_t<X, Y, Z, 8 / X, 8 / Y, 8 / Z>,                                         \
+                           cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);   \
       box_sweep_t<X, Y, Z, 8 / X, 8 / Y, 8 / Z><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks,    \
-                                                                      nblocks, inplace, gsdep, flags, ticket); \
+                                                                      nblocks, inplace, gsdep, flags, ticket, \
+                                                                      tm);                                    \
       return cudaGetLastError();                                                                              \
     }                                                                                                         \
     if (single) {                                                                                             \
+      cudaFuncSetAttribute(box_sweep_t<X, Y, Z, 1, 1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout,     \
+                           cudaSharedmemCarveoutMaxShared);                                                   \
       box_sweep_t<X, Y, Z, 1, 1, 1><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks, nblocks,       \
-                                                           inplace, gsdep, flags, ticket);                    \
+                                                           inplace, gsdep, flags, ticket, tm);                \
       return cudaGetLastError();                                                                              \
     }                                                                                                         \
   }

@@ -266,6 +266,7 @@ struct psm_plan {
   int4* d_box_regions = nullptr;
   int4* d_box_deps = nullptr;   // per block (wavefront order): own flag, -x, -y, -z predecessor flags
   int* d_box_flags = nullptr;   // GS: nboxes done-flags + one ticket
+  void* d_box_tmaps = nullptr;  // TMA tensor maps of the 8^3 region staging, 3 per patch (or null)
   int nregions = 0, reg_m[3] = {1, 1, 1};
   int box_dims[3] = {0, 0, 0};  // common block dims of all patches (0: they differ)
   std::vector<int> box_wave_off;  // blocks of wavefront w: [off[w], off[w+1])

@@ -1,7 +1,7 @@
 #!/bin/bash
 export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}  # device-sized levels
-# full ncu capture of one box-block Jacobi sweep: tools/ncu_box.sh N B OUT
-N=${1:-256}; B=${2:-8}; OUT=${3:-prof_box}
+# full ncu capture of one box-block sweep: tools/ncu_box.sh N B OUT [SCHEME]
+N=${1:-256}; B=${2:-8}; OUT=${3:-prof_box}; SCHEME=${4:-block_jacobi}
 mkdir -p gpurun_out
 cat > /tmp/box_one.py <<PY
 import sys; sys.path.insert(0, '.')
@@ -11,7 +11,7 @@ lv = ps.build_level([($N, $N, $N)])
 p = lv.patches[0]
 p.interior.copy_(torch.rand(p.interior.shape, dtype=torch.float64, device="cuda"))
 p.f.copy_(torch.randn(p.f.shape, dtype=torch.float64, device="cuda"))
-cfg = ps.SmootherConfig(scheme="block_jacobi", block_dims=($B, $B, $B))
+cfg = ps.SmootherConfig(scheme="$SCHEME", block_dims=($B, $B, $B))
 plan = _Plan(lv, cfg, ps.InverseCache())
 _run(lv, cfg, plan, 3, False, {})
 torch.cuda.synchronize()
