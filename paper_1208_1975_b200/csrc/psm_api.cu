@@ -732,6 +732,16 @@ static long long zgen_cells(const psm_plan* P, int p, int pb, int ka, int kb, in
 // Line-Jacobi sweep of planes [ka, kb) (kb < 0: all planes) of patches
 // [pa, pb): consecutive patches sharing a specialised nx run the z-marching
 // TMA kernel (one launch per group), the rest the generic tile kernel.
+// groups below this many cells take the one-tile-per-CTA specialised line
+// kernel instead of the z-marching pipeline
+static long long zmarch_min_cells() {
+  static const long long zmin = [] {
+    const char* e = getenv("PSM_ZMARCH_MIN_CELLS");
+    return e ? atoll(e) : (1LL << 21);
+  }();
+  return zmin;
+}
+
 static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, double* part, int pa, int pb, int ka,
                         int kb, cudaStream_t s) {
   const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
@@ -744,10 +754,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
     long long gcells = 0;  // cells of this group's plane range
     for (int r = p; r < q; ++r)
       gcells += (long long)P->hp[r].nx * P->hp[r].ny * ((kb < 0 ? P->hp[r].nz : kb) - ka);
-    static const long long zmin = [] {
-      const char* e = getenv("PSM_ZMARCH_MIN_CELLS");
-      return e ? atoll(e) : (1LL << 21);
-    }();
+    const long long zmin = zmarch_min_cells();
     bool peers = false;  // the fused halo lives in the z-marching kernel only
     for (int r = p; r < q; ++r) peers |= P->hp[r].iface != 0;
     if (P->tiled && line_nx_specialised(nx) && gcells < zmin && !peers) {

@@ -350,25 +350,48 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
   };
   __shared__ int gs_b, gs_nxt[2];
   const bool gsp = gsdep != nullptr;
-  // GS with TMA staging: each CTA holds two tickets, the block it computes
-  // and the next one, whose halo is prefetched into the other slot as soon
-  // as its predecessors are done (polled once while the current block
-  // computes, waited for only after the current block is released, so no
-  // CTA ever waits while holding an unreleased block)
+  // GS with TMA staging: the block's thread 0 runs a ticket pipeline off the
+  // CTA's critical path.  Besides the block it computes it holds the next
+  // ticket tA (whose halo goes to the other slot: its predecessors' flags are
+  // loaded at the top of the block and checked after the block's first and
+  // second barriers) and the one after, tB (taken at the end of the previous
+  // block, its dependencies loaded after the first barrier).  Thread 0 only
+  // ever blocks on tA after releasing the current block, and tB > tA: every
+  // unfinished ticket's predecessors are held by CTAs that make progress.
   const bool gpre = gsp && tma;
-  auto gs_ready = [&](int tk, bool block) {
-    const int4 d = gsdep[tk];
-    const int pred[3] = {d.y, d.z, d.w};
-    for (int q = 0; q < 3; ++q)
-      if (pred[q] >= 0) {
-        if (!block && box_ld_relaxed(flags + pred[q]) == 0) return false;
-        while (box_ld_relaxed(flags + pred[q]) == 0) {
-        }
-      }
+  auto gs_acquire = [&]() {
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     // the TMA reads of the halo go through the async proxy
     if (tma) asm volatile("fence.proxy.async.global;" ::: "memory");
-    return true;
+  };
+  auto gs_wait = [&](int4 d) {
+    const int pred[3] = {d.y, d.z, d.w};
+    for (int q = 0; q < 3; ++q)
+      if (pred[q] >= 0)
+        while (box_ld_relaxed(flags + pred[q]) == 0) {
+        }
+    gs_acquire();
+  };
+  const int4 kNoDeps = make_int4(-1, -1, -1, -1);
+  int tA = 0, tB = 0, fA0 = 1, fA1 = 1, fA2 = 1;
+  int4 dA = kNoDeps, dB = kNoDeps;
+  bool stgA = false;
+  auto poll_issue = [&]() {  // loads only: the values are checked later
+    fA0 = dA.y >= 0 ? box_ld_relaxed(flags + dA.y) : 1;
+    fA1 = dA.z >= 0 ? box_ld_relaxed(flags + dA.z) : 1;
+    fA2 = dA.w >= 0 ? box_ld_relaxed(flags + dA.w) : 1;
+  };
+  auto gs_hook = [&](int slot, bool first) {  // thread 0, right after a barrier of the block
+    if (tA < nblocks && !stgA) {
+      if (fA0 && fA1 && fA2) {
+        gs_acquire();
+        stage(tA, slot ^ 1);
+        stgA = true;
+      } else {
+        poll_issue();
+      }
+    }
+    if (first && tB < nblocks) dB = gsdep[tB];
   };
   if (!gsp) stage(blockIdx.x, 0);
   int slot = 0, gcur = 0;
@@ -376,10 +399,13 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
     if (tid == 0) {
       const int tk = atomicAdd(ticket, 1);
       if (tk < nblocks) {
-        gs_ready(tk, true);
+        gs_wait(gsdep[tk]);
         stage(tk, 0);
       }
       gs_b = tk;
+      tA = atomicAdd(ticket, 1);
+      dA = tA < nblocks ? gsdep[tA] : kNoDeps;
+      tB = atomicAdd(ticket, 1);
     }
     __syncthreads();
     gcur = gs_b;
@@ -392,19 +418,18 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
     if (gpre) {
       b = gcur;
       if (b >= nblocks) break;
+      if (tid == 0) {
+        gs_nxt[slot] = tA;
+        stgA = false;
+        poll_issue();
+      }
       async::bar_wait(&tbar[slot], (tphase >> slot) & 1);
       tphase ^= 1u << slot;
-      if (tid == 0) {  // next ticket; prefetch now if its predecessors are done
-        const int nt = atomicAdd(ticket, 1);
-        const bool now = nt < nblocks && gs_ready(nt, false);
-        if (now) stage(nt, slot ^ 1);
-        gs_nxt[slot] = now ? nt : -2 - nt;
-      }
     } else if (gsp) {
       slot = 0;
       if (tid == 0) {
         const int tk = atomicAdd(ticket, 1);
-        if (tk < nblocks) gs_ready(tk, true);
+        if (tk < nblocks) gs_wait(gsdep[tk]);
         gs_b = tk;
       }
       __syncthreads();
@@ -461,6 +486,7 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
         }
       }
       __syncthreads();
+      if (gpre && tid == 0) gs_hook(slot, true);
     }
     if constexpr (MX * BX == 8 && MY * BY == 8 && MZ * BZ == 8) {
       if (interior8) {
@@ -528,6 +554,7 @@ PSM_BOX_A(1)
         // every warp is past this region's halo reads of the previous slot:
         // prefetch the next region into it
         if (tma && !gsp) stage(b + gridDim.x, slot ^ 1);
+        if (gpre && tid == 0) gs_hook(slot, true);
         // z pass (plane j = 2 warp + tt, line i = lr), scaled by 1/lambda;
         // z -> z' by shuffle: lane needs (k = 4 ks + lc, i = box_ip(lr))
 PSM_BOX_A(2)
@@ -553,6 +580,7 @@ PSM_BOX_A(3)
           for (int e = 0; e < 2; ++e) wc[lr * kRp + (2 * warp + tt) * kRs + box_ip(2 * lc + e)] = d[tt][e];
         }
         __syncthreads();
+        if (gpre && tid == 0) gs_hook(slot, false);
         // y' pass (plane k = 2 warp + tt, line i = lr); y' -> x' by shuffle:
         // lane needs (j = lr, i = 4 ks + lc)
 PSM_BOX_A(4)
@@ -667,17 +695,19 @@ PSM_BOX_A(5)
     // second barrier are warp-local and the next prefetch waited for the
     // first; edge regions, the cp.async staging and the GS release do
     if (!interior8 || !tma || gsp) __syncthreads();
-    if (gsp && tid == 0) {  // every thread's stores precede the barrier above: release them
-      __threadfence();
+    if (gsp && tid == 0)  // every thread's stores precede the barrier above: the release covers them
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + gsdep[b].x), "r"(1) : "memory");
-    }
     if (gpre) {
-      const int code = gs_nxt[slot];
-      gcur = code >= 0 ? code : -2 - code;
-      if (code < 0 && tid == 0 && gcur < nblocks) {  // not prefetched: wait now (this block is released)
-        gs_ready(gcur, true);
-        stage(gcur, slot ^ 1);
+      if (tid == 0) {
+        if (tA < nblocks && !stgA) {  // not prefetched: wait now (this block is released)
+          gs_wait(dA);
+          stage(tA, slot ^ 1);
+        }
+        tA = tB;
+        dA = dB;
+        tB = atomicAdd(ticket, 1);
       }
+      gcur = gs_nxt[slot];
     }
   }
 }

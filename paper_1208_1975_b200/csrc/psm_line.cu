@@ -259,6 +259,9 @@ __global__ void line_apply_kernel(const LineFac* __restrict__ L, const double* _
 //   C  8 cells per thread: x = y - cl*g[i] - cr*h[i], v = u + omega*x,
 //      store v and the physical x-face ghosts of v.
 // Shared buffers are double-buffered across tiles: two barriers per tile.
+// At small sizes a tile is a latency chain (tools/nx_timing_probe.py, built
+// with -DPSM_NX_TIMING: A 3.5 us, B 0.8 us, C 1.7-2.7 us at 64^3), so every
+// independent load of phase A is issued before the first use of any.
 // ---------------------------------------------------------------------------
 template <int NX, int UNIT>
 __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* __restrict__ patches, int npatch,
@@ -277,35 +280,27 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
   const LineFac* lf_loaded = nullptr;
   double lo = 0, up = 0, up_h31 = 0, lo_g0 = 0, d_full = 0;
   int buf = 0;
+#ifdef PSM_NX_TIMING
+  unsigned long long tm0 = 0, tm1 = 0, tm2 = 0, tmA = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tmA));
+#endif
   for (long long tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x, buf ^= 1) {
+#ifdef PSM_NX_TIMING
+    if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm0));
+#endif
     const int pi = find_patch(patches, npatch, tile);
     const PatchDev& P = patches[pi];
-    const LineFac* L = P.lf;
-    if (L != lf_loaded) {  // uniform across the CTA; tables for this nx
-      __syncthreads();
-      if (tid < kSeg) {
-        const double im = L->invm[tid];
-        tab_invm[tid] = im;
-        tab_loinv[tid] = L->lo * im;
-        tab_cp[tid] = L->cp[tid];
-        tab_g[tid] = L->g[tid];
-        tab_h[tid] = L->h[tid];
-      }
-      lo = L->lo;
-      up = L->up;
-      up_h31 = L->up_h31;
-      lo_g0 = L->lo_g0;
-      d_full = L->d_full;
-      lf_loaded = L;
-      __syncthreads();
-    }
+    // independent loads first (the tile's latency is a chain of L2 round
+    // trips at small sizes): the active flag and both buffer pointers
+    const int act = active[pi];
+    double* const b0 = P.buf[0];
+    double* const b1 = P.buf[1];
     const int ny = P.ny;
     int k, j0, rows;
     tile_coords(P, tile, k, j0, rows);
     const long long pxy = (long long)PX * (ny + 2);
-    const int act = active[pi];
-    const double* __restrict__ u = P.buf[act];
-    double* __restrict__ v = P.buf[act ^ 1];
+    const double* __restrict__ u = act ? b1 : b0;
+    double* __restrict__ v = act ? b0 : b1;
     const long long ubase = (long long)(k + 1) * pxy + (long long)(j0 + 1) * PX + 1;
     const double* __restrict__ fb = P.f + ((long long)k * ny + j0) * NX;
     double* __restrict__ rb = rs[buf];
@@ -315,7 +310,7 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
     double ucen[E];
 #pragma unroll
     for (int h = 0; h < E; h += 4) {
-      double c[4], ym[4], yp[4], zm[4], zp[4], fv[4];
+      double c[4], ym[4], yp[4], zm[4], zp[4], fv[4], xe[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = (h + q) * T + tid;
@@ -328,8 +323,10 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
           zm[q] = __ldg(u + iu - pxy);
           zp[q] = __ldg(u + iu + pxy);
           fv[q] = __ldg(fb + e);
+          // the warp's outer x neighbours, issued with the rest
+          xe[q] = lane == 0 ? __ldg(u + iu - 1) : lane == 31 ? __ldg(u + iu + 1) : 0.0;
         } else {
-          c[q] = ym[q] = yp[q] = zm[q] = zp[q] = fv[q] = 0.0;
+          c[q] = ym[q] = yp[q] = zm[q] = zp[q] = fv[q] = xe[q] = 0.0;
         }
       }
 #pragma unroll
@@ -340,9 +337,8 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
         double xr = __shfl_down_sync(0xffffffffu, c[q], 1);
         ucen[h + q] = c[q];
         if (row < rows) {
-          const long long iu = ubase + (long long)row * PX + x;
-          if (lane == 0) xl = __ldg(u + iu - 1);
-          if (lane == 31) xr = __ldg(u + iu + 1);
+          if (lane == 0) xl = xe[q];
+          if (lane == 31) xr = xe[q];
           double res;
           if (UNIT) {
             double acc = __dmul_rn(st.c, c[q]);
@@ -361,10 +357,31 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
         }
       }
     }
+    const LineFac* L = P.lf;
+    if (L != lf_loaded) {  // uniform across the CTA; tables for this nx (used from phase B on)
+      __syncthreads();     // (the previous tile's phase C may still read them)
+      if (tid < kSeg) {
+        const double im = L->invm[tid];
+        tab_invm[tid] = im;
+        tab_loinv[tid] = L->lo * im;
+        tab_cp[tid] = L->cp[tid];
+        tab_g[tid] = L->g[tid];
+        tab_h[tid] = L->h[tid];
+      }
+      lo = L->lo;
+      up = L->up;
+      up_h31 = L->up_h31;
+      lo_g0 = L->lo_g0;
+      d_full = L->d_full;
+      lf_loaded = L;
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
     if (lane == 0) wsum[buf][warp] = ssq;
     __syncthreads();  // (1) r complete
+#ifdef PSM_NX_TIMING
+    if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm1));
+#endif
     if (tid == 0 && partials) {
       double t = 0.0;
 #pragma unroll
@@ -404,6 +421,9 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
       cr[buf][tid] = cr_v;
     }
     __syncthreads();  // (2) y, cl, cr complete
+#ifdef PSM_NX_TIMING
+    if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm2));
+#endif
 
     // ---- C ----------------------------------------------------------------
     const bool yz_edge = j0 == 0 || j0 + rows >= ny || k == 0 || k == P.nz - 1;  // tile touches a y/z face
@@ -427,6 +447,14 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
         }
       }
     }
+#ifdef PSM_NX_TIMING
+    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 77)) {
+      unsigned long long t3;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+      printf("nx-timing cta %d tile %lld: since-start %llu  A %llu  B %llu  C %llu ns\n", blockIdx.x, tile,
+             tm0 - tmA, tm1 - tm0, tm2 - tm1, t3 - tm2);
+    }
+#endif
   }
 }
 
@@ -470,14 +498,17 @@ cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch
   if (t1 <= t0) return cudaSuccess;
   const long long n = t1 - t0;
   if (grid > n) grid = (int)n;
+#define PSM_NX(N) \
+  case N: return launch_nx<N>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
   switch (nx) {
-    case 64: return launch_nx<64>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
-    case 128: return launch_nx<128>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
-    case 256: return launch_nx<256>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
-    case 512: return launch_nx<512>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
-    case 1024: return launch_nx<1024>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+    PSM_NX(64)
+    PSM_NX(128)
+    PSM_NX(256)
+    PSM_NX(512)
+    PSM_NX(1024)
     default: return cudaErrorInvalidValue;
   }
+#undef PSM_NX
 }
 
 // ---- host-side launchers ---------------------------------------------------

@@ -1,7 +1,9 @@
-"""Parity at the exact BASELINE.json configurations (C2, C3, C4 and the
+"""Parity at the exact BASELINE.json configurations (C1, C2, C3, C4 and the
 north-star 512^3 line-Jacobi grid), through the public API and so through
 libpsmooth.so, against the CPU restatement of the reference:
 
+* C1  64^3 single patch, line Jacobi over 10 sweeps (and two more small
+  shapes) against the serial restatement;
 * C2  256^3 single patch, line GS: wavefront ("colour-ordered") mode within
   1e-12 of the serial lexicographic sweep (iterates and history) over 2
   sweeps; chaotic mode's per-sweep residual factor within 2% of the serial
@@ -79,6 +81,20 @@ def test_c2_chaotic_line_gs_256_ten_sweeps():
     hist = _device_smooth(g, "chaotic_block_gs", (256, 1, 1), 10, "chaotic")
     assert len(hist) == 11
     _assert_factors(hist, want)
+
+
+# ---------------------------------------------------------------- C1
+@pytest.mark.parametrize("shape,steps", [((64, 64, 64), 10), ((128, 64, 32), 3), ((64, 96, 40), 5)])
+def test_c1_small_line_jacobi(shape, steps):
+    """Small single-patch levels (the one-tile-per-CTA line kernel):
+    iterates and every history entry against the serial restatement, odd
+    and even sweep counts (final buffer parity)."""
+    o, g = _levels((1, 1, 1), shape)
+    want = cport.line_smooth(o, "block_jacobi", steps=steps)
+    hist = _device_smooth(g, "block_jacobi", (shape[0], 1, 1), steps)
+    assert len(hist) == steps + 1
+    _assert_iterates(o, g)
+    assert G.hist_rel(hist, want) < TOL
 
 
 # ---------------------------------------------------------------- C3
