@@ -35,7 +35,7 @@ cudaError_t launch_line_zgen(const int* nxs, int nnx, int unit, const PatchDev* 
                              int grid, const LineFac& L, cudaStream_t stream);
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
-                           cudaStream_t stream);
+                           const LineFac& L, cudaStream_t stream);
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
                                    long long max_face, int skip_x, int use_covered, cudaStream_t stream);
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
@@ -768,7 +768,7 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
         const int a = ka, b = (kb < 0) ? h.nz : kb;
         const long long t0 = h.tile0 + (long long)a * h.tpp, t1 = h.tile0 + (long long)b * h.tpp;
         CUDA_TRY(launch_line_nx(nx, unit ? 1 : 0, P->d_patches, P->npatch, da, P->st, omega, part, t0, t1,
-                                line_nx_occupancy(nx) * sms, s));
+                                line_nx_occupancy(nx) * sms, P->fac[r]->h_line, s));
         P->launches += 1;
       }
     } else if (P->tiled && line_nx_specialised(nx) && P->hp[p].R == zmarch_rows(nx)) {

@@ -265,7 +265,7 @@ __device__ __forceinline__ double box_shfl_pick(const double (&d)[2], int src, i
   return e ? v1 : v0;
 }
 
-template <int BX, int BY, int BZ, int MX, int MY, int MZ>
+template <int BX, int BY, int BZ, int MX, int MY, int MZ, int GS>
 __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDev* __restrict__ patches,
                                                      const unsigned char* __restrict__ active, StencilDev st,
                                                      double omega, const int4* __restrict__ blocks, int nblocks,
@@ -297,14 +297,18 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
     }
     __syncthreads();
   }
+  // one thread: the TMA copies of region B (active buffer act) into a slot
+  auto stage_tma = [&](int slot, int4 B, int act) {
+    const char* m = tmaps + (size_t)(3 * B.x) * kTmapBytes;
+    async::bar_expect(&tbar[slot], (uint32_t)((kHp * kHs + FN) * sizeof(double)));
+    async::tensor3d_g2s(&hbuf[slot][0], m + act * kTmapBytes, B.y, B.z, B.w, &tbar[slot]);
+    async::tensor3d_g2s(&fbuf[slot][0], m + 2 * kTmapBytes, B.y, B.z, B.w, &tbar[slot]);
+  };
   auto stage = [&](int b, int slot) {
     if (tma) {
       if (tid == 0 && b < nblocks) {
         const int4 B = blocks[b];
-        const char* m = tmaps + (size_t)(3 * B.x) * kTmapBytes;
-        async::bar_expect(&tbar[slot], (uint32_t)((kHp * kHs + FN) * sizeof(double)));
-        async::tensor3d_g2s(&hbuf[slot][0], m + active[B.x] * kTmapBytes, B.y, B.z, B.w, &tbar[slot]);
-        async::tensor3d_g2s(&fbuf[slot][0], m + 2 * kTmapBytes, B.y, B.z, B.w, &tbar[slot]);
+        stage_tma(slot, B, active[B.x]);
       }
       return;
     }
@@ -349,7 +353,7 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
     box_commit();
   };
   __shared__ int gs_b, gs_nxt[2];
-  const bool gsp = gsdep != nullptr;
+  const bool gsp = GS && gsdep != nullptr;  // (GS = 0: the persistent-GS code compiles away)
   // GS with TMA staging: the block's thread 0 runs a ticket pipeline off the
   // CTA's critical path.  Besides the block it computes it holds the next
   // ticket tA (whose halo goes to the other slot: its predecessors' flags are
@@ -373,8 +377,8 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
     gs_acquire();
   };
   const int4 kNoDeps = make_int4(-1, -1, -1, -1);
-  int tA = 0, tB = 0, fA0 = 1, fA1 = 1, fA2 = 1;
-  int4 dA = kNoDeps, dB = kNoDeps;
+  int tA = 0, tB = 0, fA0 = 1, fA1 = 1, fA2 = 1, aA = 0;
+  int4 dA = kNoDeps, dB = kNoDeps, bA = kNoDeps, bB = kNoDeps;  // deps and region of tA / tB
   bool stgA = false;
   auto poll_issue = [&]() {  // loads only: the values are checked later
     fA0 = dA.y >= 0 ? box_ld_relaxed(flags + dA.y) : 1;
@@ -385,13 +389,16 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
     if (tA < nblocks && !stgA) {
       if (fA0 && fA1 && fA2) {
         gs_acquire();
-        stage(tA, slot ^ 1);
+        stage_tma(slot ^ 1, bA, aA);
         stgA = true;
       } else {
         poll_issue();
       }
     }
-    if (first && tB < nblocks) dB = gsdep[tB];
+    if (first && tB < nblocks) {  // loads for the ticket after next, used at the end of the block
+      dB = gsdep[tB];
+      bB = blocks[tB];
+    }
   };
   if (!gsp) stage(blockIdx.x, 0);
   int slot = 0, gcur = 0;
@@ -404,7 +411,11 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
       }
       gs_b = tk;
       tA = atomicAdd(ticket, 1);
-      dA = tA < nblocks ? gsdep[tA] : kNoDeps;
+      if (tA < nblocks) {
+        dA = gsdep[tA];
+        bA = blocks[tA];
+        aA = active[bA.x];
+      }
       tB = atomicAdd(ticket, 1);
     }
     __syncthreads();
@@ -701,10 +712,12 @@ PSM_BOX_A(5)
       if (tid == 0) {
         if (tA < nblocks && !stgA) {  // not prefetched: wait now (this block is released)
           gs_wait(dA);
-          stage(tA, slot ^ 1);
+          stage_tma(slot ^ 1, bA, aA);
         }
         tA = tB;
         dA = dB;
+        bA = bB;
+        if (tA < nblocks) aA = active[bA.x];
         tB = atomicAdd(ticket, 1);
       }
       gcur = gs_nxt[slot];
@@ -814,23 +827,19 @@ cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* activ
   const bool region = mx * bx == 8 && my * by == 8 && mz * bz == 8;  // Jacobi regions of 8^3
   const bool single = mx == 1 && my == 1 && mz == 1;
   const char* tm = (const char*)tmaps;
-#define PSM_BOXT(X, Y, Z)                                                                                      \
-  if (bx == X && by == Y && bz == Z) {                                                                        \
-    if (region) {                                                                                             \
-      cudaFuncSetAttribute(box_sweep_t<X, Y, Z, 8 / X, 8 / Y, 8 / Z>,                                         \
-                           cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);   \
-      box_sweep_t<X, Y, Z, 8 / X, 8 / Y, 8 / Z><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks,    \
-                                                                      nblocks, inplace, gsdep, flags, ticket, \
-                                                                      tm);                                    \
-      return cudaGetLastError();                                                                              \
-    }                                                                                                         \
-    if (single) {                                                                                             \
-      cudaFuncSetAttribute(box_sweep_t<X, Y, Z, 1, 1, 1>, cudaFuncAttributePreferredSharedMemoryCarveout,     \
-                           cudaSharedmemCarveoutMaxShared);                                                   \
-      box_sweep_t<X, Y, Z, 1, 1, 1><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks, nblocks,       \
-                                                           inplace, gsdep, flags, ticket, tm);                \
-      return cudaGetLastError();                                                                              \
-    }                                                                                                         \
+#define PSM_BOXK(X, Y, Z, M1, M2, M3, G)                                                                     \
+  {                                                                                                           \
+    cudaFuncSetAttribute(box_sweep_t<X, Y, Z, M1, M2, M3, G>, cudaFuncAttributePreferredSharedMemoryCarveout, \
+                         cudaSharedmemCarveoutMaxShared);                                                     \
+    box_sweep_t<X, Y, Z, M1, M2, M3, G><<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks, nblocks,   \
+                                                               inplace, gsdep, flags, ticket, tm);            \
+    return cudaGetLastError();                                                                                \
+  }
+#define PSM_BOXT(X, Y, Z)                                      \
+  if (bx == X && by == Y && bz == Z) {                        \
+    if (region && !gsdep) PSM_BOXK(X, Y, Z, 8 / X, 8 / Y, 8 / Z, 0) \
+    if (single && gsdep) PSM_BOXK(X, Y, Z, 1, 1, 1, 1)        \
+    if (single) PSM_BOXK(X, Y, Z, 1, 1, 1, 0)                 \
   }
   PSM_BOXT(2, 2, 2)
   PSM_BOXT(4, 2, 2)
@@ -840,6 +849,7 @@ cudaError_t launch_box_sweep(const PatchDev* patches, const unsigned char* activ
   PSM_BOXT(8, 8, 4)
   PSM_BOXT(8, 8, 8)
 #undef PSM_BOXT
+#undef PSM_BOXK
   box_sweep_kernel<<<grid, kBoxT, 0, s>>>(patches, active, st, omega, blocks, nblocks, inplace, mx, my, mz);
   return cudaGetLastError();
 }

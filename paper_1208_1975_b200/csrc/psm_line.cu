@@ -263,22 +263,36 @@ __global__ void line_apply_kernel(const LineFac* __restrict__ L, const double* _
 // with -DPSM_NX_TIMING: A 3.5 us, B 0.8 us, C 1.7-2.7 us at 64^3), so every
 // independent load of phase A is issued before the first use of any.
 // ---------------------------------------------------------------------------
+#ifndef PSM_NX_THREADS
+#define PSM_NX_THREADS 512
+#endif
+constexpr int kNxT = PSM_NX_THREADS;  // threads per tile CTA (cells per thread: 2048 / kNxT)
 template <int NX, int UNIT>
-__global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* __restrict__ patches, int npatch,
+__global__ void __launch_bounds__(kNxT, 512 / kNxT) line_jacobi_nx_kernel(const PatchDev* __restrict__ patches, int npatch,
                                                                 const unsigned char* __restrict__ active,
                                                                 StencilDev st, double omega,
                                                                 double* __restrict__ partials, long long tile_begin,
-                                                                long long tile_end) {
-  constexpr int T = 256, R = kMaxTileCells / NX, NSEG = NX / kSeg, CELLS = R * NX, E = CELLS / T;
+                                                                long long tile_end, const __grid_constant__ LineFac L) {
+  constexpr int T = kNxT, R = kMaxTileCells / NX, NSEG = NX / kSeg, CELLS = R * NX, E = CELLS / T;
   constexpr int RS = NX + NSEG, PX = NX + 2, NSL = R * NSEG;
-  static_assert(E == 8 && NSEG <= 32 && NSL <= T, "tile shape");
+  static_assert((E == 8 || E == 4) && NSEG <= 32 && NSL <= T, "tile shape");
   __shared__ double rs[2][R * RS];
   __shared__ double cl[2][NSL], cr[2][NSL];
   __shared__ double wsum[2][T / 32];
   __shared__ double tab_invm[kSeg], tab_loinv[kSeg], tab_cp[kSeg], tab_g[kSeg], tab_h[kSeg];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const LineFac* lf_loaded = nullptr;
-  double lo = 0, up = 0, up_h31 = 0, lo_g0 = 0, d_full = 0;
+  // the line factors come in as a kernel parameter (constant bank): no
+  // global round trip before the first tile
+  if (tid < kSeg) {
+    const double im = L.invm[tid];
+    tab_invm[tid] = im;
+    tab_loinv[tid] = L.lo * im;
+    tab_cp[tid] = L.cp[tid];
+    tab_g[tid] = L.g[tid];
+    tab_h[tid] = L.h[tid];
+  }
+  const double lo = L.lo, up = L.up, up_h31 = L.up_h31, lo_g0 = L.lo_g0, d_full = L.d_full;
+  __syncthreads();
   int buf = 0;
 #ifdef PSM_NX_TIMING
   unsigned long long tm0 = 0, tm1 = 0, tm2 = 0, tmA = 0;
@@ -357,24 +371,6 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
         }
       }
     }
-    const LineFac* L = P.lf;
-    if (L != lf_loaded) {  // uniform across the CTA; tables for this nx (used from phase B on)
-      __syncthreads();     // (the previous tile's phase C may still read them)
-      if (tid < kSeg) {
-        const double im = L->invm[tid];
-        tab_invm[tid] = im;
-        tab_loinv[tid] = L->lo * im;
-        tab_cp[tid] = L->cp[tid];
-        tab_g[tid] = L->g[tid];
-        tab_h[tid] = L->h[tid];
-      }
-      lo = L->lo;
-      up = L->up;
-      up_h31 = L->up_h31;
-      lo_g0 = L->lo_g0;
-      d_full = L->d_full;
-      lf_loaded = L;
-    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
     if (lane == 0) wsum[buf][warp] = ssq;
@@ -448,11 +444,11 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
       }
     }
 #ifdef PSM_NX_TIMING
-    if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == 77)) {
+    if (tid == 0) {
       unsigned long long t3;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
-      printf("nx-timing cta %d tile %lld: since-start %llu  A %llu  B %llu  C %llu ns\n", blockIdx.x, tile,
-             tm0 - tmA, tm1 - tm0, tm2 - tm1, t3 - tm2);
+      printf("nx-timing cta %d tile %lld: start %llu end %llu  A %llu  B %llu  C %llu ns\n", blockIdx.x, tile, tmA,
+             t3, tm1 - tm0, tm2 - tm1, t3 - tm2);
     }
 #endif
   }
@@ -461,11 +457,11 @@ __global__ void __launch_bounds__(256, 2) line_jacobi_nx_kernel(const PatchDev* 
 template <int NX>
 static cudaError_t launch_nx(int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                              const StencilDev& st, double omega, double* partials, long long t0, long long t1,
-                             int grid, cudaStream_t stream) {
+                             int grid, const LineFac& L, cudaStream_t stream) {
   if (unit)
-    line_jacobi_nx_kernel<NX, 1><<<grid, 256, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1);
+    line_jacobi_nx_kernel<NX, 1><<<grid, kNxT, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1, L);
   else
-    line_jacobi_nx_kernel<NX, 0><<<grid, 256, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1);
+    line_jacobi_nx_kernel<NX, 0><<<grid, kNxT, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1, L);
   return cudaGetLastError();
 }
 
@@ -475,11 +471,14 @@ bool line_nx_specialised(int nx) {
 }
 
 template <int NX>
-static int occ_nx() {
-  int a = 0, b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, line_jacobi_nx_kernel<NX, 0>, 256, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, line_jacobi_nx_kernel<NX, 1>, 256, 0);
-  return a < b ? a : b;
+static int occ_nx() {  // (per process: every device of a run is the same sm_100a part)
+  static const int occ = [] {
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, line_jacobi_nx_kernel<NX, 0>, kNxT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, line_jacobi_nx_kernel<NX, 1>, kNxT, 0);
+    return a < b ? a : b;
+  }();
+  return occ;
 }
 
 int line_nx_occupancy(int nx) {
@@ -494,12 +493,12 @@ int line_nx_occupancy(int nx) {
 
 cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
                            const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
-                           cudaStream_t stream) {
+                           const LineFac& L, cudaStream_t stream) {
   if (t1 <= t0) return cudaSuccess;
   const long long n = t1 - t0;
   if (grid > n) grid = (int)n;
 #define PSM_NX(N) \
-  case N: return launch_nx<N>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, stream);
+  case N: return launch_nx<N>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, L, stream);
   switch (nx) {
     PSM_NX(64)
     PSM_NX(128)

@@ -2,7 +2,8 @@
 
 One "step" is what the reference's smoother step does (smoother.py:138-169):
 the sweep plus the ghost refresh, without history.  Timed with CUDA events on
-the current stream over K steps after W warm-up steps; prints one JSON line
+the current stream over K steps in graph replay (the steady state of repeated
+smooth() calls) after W warm-up steps; prints one JSON line
 per (config, scheme) with updates/s, GB/s at the 24 B/update algorithmic
 traffic, and for plane blocks the algorithmic fp64 TFLOP/s.
 
@@ -39,8 +40,14 @@ def plane_flops(nx):
 
 
 def time_steps(level, cfg, steps, warmup):
+    """Device time per step of a `steps`-step sequence in its steady state:
+    the first call with a new step count runs eagerly, the second captures
+    the CUDA graph, the timed third call replays it (as repeated smooth()
+    calls do)."""
     plan = _Plan(level, cfg, ps.InverseCache())
     ps.smoother._run(level, cfg, plan, warmup, False, None)
+    for _ in range(2):
+        _run(level, cfg, plan, steps, False, None)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

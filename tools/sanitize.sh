@@ -19,7 +19,7 @@ EXTRA="--chaotic" run memcheck --leak-check no
 # racecheck one case at a time, so each kernel family gets its own summary
 for c in zmarch_line_jacobi zmarch_line_jacobi_256 zgen_line_jacobi odd_line_jacobi gs_pipe_wavefront gs_pipe_odd_nx \
          plane_band_jacobi plane_gs plane_gs_mixed box_jacobi box_gs ghosts_lattice_jacobi gs_multisweep \
-         plane_gs_dst_chain plane_jacobi_dst box_gs_persistent api_primitives; do
+         plane_gs_dst_chain plane_jacobi_dst box_gs_persistent api_primitives box_jacobi_4 box_jacobi_odd; do
   EXTRA="--only $c" run racecheck --racecheck-report hazard --print-limit 4
 done
 EXTRA="--chaotic" run synccheck

@@ -75,6 +75,10 @@ CASES = {
     "box_gs_persistent": lambda: run("box_gs_persistent", level([((24, 16, 16), (0, 0, 0))]), "chaotic_block_gs",
                                      (8, 8, 8)),
     "api_primitives": lambda: api_primitives(),
+    # box sweep: TMA staging + fragment-register passes (4^3 blocks in 8^3
+    # regions), and the cp.async fallback of an odd-width patch
+    "box_jacobi_4": lambda: run("box_jacobi_4", level([((24, 16, 13), (0, 0, 0))]), "block_jacobi", (4, 4, 4)),
+    "box_jacobi_odd": lambda: run("box_jacobi_odd", level([((21, 16, 16), (0, 0, 0))]), "block_jacobi", (8, 8, 8)),
 }
 
 
