@@ -357,9 +357,9 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
   // GS with TMA staging: the block's thread 0 runs a ticket pipeline off the
   // CTA's critical path.  Besides the block it computes it holds the next
   // ticket tA (whose halo goes to the other slot: its predecessors' flags are
-  // loaded at the top of the block and checked after the block's first and
-  // second barriers) and the one after, tB (taken at the end of the previous
-  // block, its dependencies loaded after the first barrier).  Thread 0 only
+  // loaded at the end of the previous block and checked after this block's
+  // first and second barriers) and the one after, tB (taken at the end of
+  // the previous block, its dependencies loaded after the first barrier).  Thread 0 only
   // ever blocks on tA after releasing the current block, and tB > tA: every
   // unfinished ticket's predecessors are held by CTAs that make progress.
   const bool gpre = gsp && tma;
@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
         aA = active[bA.x];
       }
       tB = atomicAdd(ticket, 1);
+      poll_issue();
     }
     __syncthreads();
     gcur = gs_b;
@@ -432,7 +433,6 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
       if (tid == 0) {
         gs_nxt[slot] = tA;
         stgA = false;
-        poll_issue();
       }
       async::bar_wait(&tbar[slot], (tphase >> slot) & 1);
       tphase ^= 1u << slot;
@@ -718,6 +718,7 @@ PSM_BOX_A(5)
         dA = dB;
         bA = bB;
         if (tA < nblocks) aA = active[bA.x];
+        poll_issue();  // checked after the next block's first barrier
         tB = atomicAdd(ticket, 1);
       }
       gcur = gs_nxt[slot];

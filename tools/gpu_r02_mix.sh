@@ -1,12 +1,14 @@
 #!/bin/bash
-# box tests + F1 timing; small-level line kernel launch timeline (globaltimer variant)
+# box GS pipeline tweak (tests + F1); band kernel thread-count variants (C3/C4 plane Jacobi)
 export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}
-export PATH=/usr/local/cuda/bin:$PATH
 O=gpurun_out; mkdir -p $O
 make -j all > $O/build.log 2>&1 || { echo build failed; tail $O/build.log; exit 1; }
-timeout -s KILL 900 python -m pytest tests -m gpu -x -q -k "box or Box or f1 or F1 or api or smoke" > $O/box_tests.log 2>&1; echo "box tests rc=$?"; tail -2 $O/box_tests.log
-timeout -s KILL 600 python tools/bench_configs.py --only F1 > $O/f1.jsonl 2>&1; cut -c150-400 $O/f1.jsonl
-mkdir -p build/variant
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DPSM_NX_TIMING -c -o build/variant/psm_line_t.o paper_1208_1975_b200/csrc/psm_line.cu && \
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variant/libpsmooth_t.so $(ls build/obj/*.o | grep -v psm_line.o) build/variant/psm_line_t.o -lcudart && \
-PSM_LIB=$PWD/build/variant/libpsmooth_t.so python tools/nx_timing_probe.py 2>&1 | tail -6
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q -k "box or Box or f1 or F1" > $O/box_tests.log 2>&1; echo "box tests rc=$?"; tail -2 $O/box_tests.log
+timeout -s KILL 600 python tools/bench_configs.py --only F1 --runs 0,3 > $O/f1.jsonl 2>&1; cut -c150-400 $O/f1.jsonl
+for T in 64 128 256; do
+  L=$PWD/build/variant/libpsmooth_band$T.so; [ $T = 64 ] && L=$PWD/paper_1208_1975_b200/libpsmooth.so
+  echo "== band T=$T"
+  PSM_LIB=$L timeout -s KILL 600 python tools/bench_configs.py --only C3 --runs 0 2>&1 | cut -c150-400
+  PSM_LIB=$L timeout -s KILL 600 python tools/bench_configs.py --only F3 --runs 3 2>&1 | cut -c150-400
+done
+PSM_LIB=$PWD/build/variant/libpsmooth_band128.so timeout -s KILL 900 python -m pytest tests -m gpu -x -q -k "plane" > $O/band128_tests.log 2>&1; echo "band128 plane tests rc=$?"; tail -2 $O/band128_tests.log
