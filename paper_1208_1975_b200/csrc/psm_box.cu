@@ -259,10 +259,18 @@ __device__ __forceinline__ void box_mma2(const double (&a)[2], const double (&bq
   box_dmma(d[0], d[1], a[0], bq[0]);
   box_dmma(d[0], d[1], a[1], bq[1]);
 }
-// (e ? v1 : v0) of lane src
-__device__ __forceinline__ double box_shfl_pick(const double (&d)[2], int src, int e) {
-  const double v0 = __shfl_sync(0xffffffffu, d[0], src), v1 = __shfl_sync(0xffffffffu, d[1], src);
-  return e ? v1 : v0;
+// One register exchange between passes: every lane needs two of the 64
+// values its warp holds (two per lane).  Two shuffles suffice: in each, every
+// lane sends the element (pick ? d[1] : d[0], then the other) that its one
+// reader needs and reads from src0 / src1; `swap` says which received value
+// is the lane's ks = 0 operand.  tools/box_lanes_sim.py derives and checks
+// the three schedules (x -> y, z -> z', y' -> x').
+__device__ __forceinline__ void box_exchange(const double (&d)[2], bool pick, int src0, int src1, bool swap,
+                                             double (&bq)[2]) {
+  const double s0 = __shfl_sync(0xffffffffu, pick ? d[1] : d[0], src0);
+  const double s1 = __shfl_sync(0xffffffffu, pick ? d[0] : d[1], src1);
+  bq[0] = swap ? s1 : s0;
+  bq[1] = swap ? s0 : s1;
 }
 
 template <int BX, int BY, int BZ, int MX, int MY, int MZ, int GS>
@@ -546,15 +554,14 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
 PSM_BOX_A(0)
         #pragma unroll
         for (int tt = 0; tt < 2; ++tt) box_mma2(A0, bq[tt], d[tt]);
+        {  // lane (lr, lc) reads lane (box_ip(lr), {0,2,1,3}[lc]) then (.., {1,3,0,2}[lc])
+          const int s0 = box_ip(lr) * 4 + (((lc & 1) << 1) | (lc >> 1));
 #pragma unroll
-        for (int tt = 0; tt < 2; ++tt)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const int ns = 2 * ks + (lc >> 1) + 4 * (lc & 1);  // x-pass line of row j = 4 ks + lc
-            bq[tt][ks] = box_shfl_pick(d[tt], box_ip(lr) * 4 + (ns >> 1), ns & 1);
-          }
+          for (int tt = 0; tt < 2; ++tt) box_exchange(d[tt], lc & 1, s0, s0 ^ 1, lc >> 1, bq[tt]);
+        }
         // y pass -> cube (k = 2 warp + tt, j = lr, i = box_ip(2 lc + e))
 PSM_BOX_A(1)
+        __syncwarp();  // the warp's y'-pass cube reads of the previous region precede these stores
         #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
           box_mma2(A1, bq[tt], d[tt]);
@@ -577,13 +584,15 @@ PSM_BOX_A(2)
           d[tt][0] *= scl[tt][0];
           d[tt][1] *= scl[tt][1];
         }
-        const int ir = box_ip(lr);
+        {  // lane reads row k = lc or 4 + lc (first the one of its own parity e) at column box_ip(lr) / 2
+          const int ir = box_ip(lr), e = ir & 1;
+          const int s0 = ((e ? 4 : 0) + lc) * 4 + (ir >> 1), s1 = ((e ? 0 : 4) + lc) * 4 + (ir >> 1);
 #pragma unroll
-        for (int tt = 0; tt < 2; ++tt)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = box_shfl_pick(d[tt], (4 * ks + lc) * 4 + (ir >> 1), ir & 1);
+          for (int tt = 0; tt < 2; ++tt) box_exchange(d[tt], lr >= 4, s0, s1, e, bq[tt]);
+        }
         // z' pass -> cube (k = lr, j = 2 warp + tt, i = box_ip(2 lc + e))
 PSM_BOX_A(3)
+        __syncwarp();  // the warp's z-pass cube reads precede these stores (WAR across lanes)
         #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
           box_mma2(A3, bq[tt], d[tt]);
@@ -601,10 +610,11 @@ PSM_BOX_A(4)
           for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = wc[(2 * warp + tt) * kRp + (4 * ks + lc) * kRs + lr];
           box_mma2(A4, bq[tt], d[tt]);
         }
+        {  // within the quad: columns (lc >> 1) + 2 (lc & 1), then (lc >> 1) + 2 (1 - (lc & 1))
+          const int s0 = lr * 4 + (lc >> 1) + 2 * (lc & 1), s1 = lr * 4 + (lc >> 1) + 2 * ((lc & 1) ^ 1);
 #pragma unroll
-        for (int tt = 0; tt < 2; ++tt)
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) bq[tt][ks] = box_shfl_pick(d[tt], lr * 4 + ((4 * ks + lc) >> 1), lc & 1);
+          for (int tt = 0; tt < 2; ++tt) box_exchange(d[tt], lc >> 1, s0, s1, lc & 1, bq[tt]);
+        }
         // x' pass: result (i = lr, j = 2 lc + e, k = 2 warp + tt); relax and store
 PSM_BOX_A(5)
         #pragma unroll

@@ -48,12 +48,15 @@ for w in range(4):
         check('res hb',[ (k+1)*HP+(Jx(l>>2)+1)*HS+4*ks+(l&3)+1+off for l in range(32)])
       check('res f',[ (k*8+Jx(l>>2))*FS+4*ks+(l&3) for l in range(32)])
     dx=dmma(M[0],bx)
+    # x -> y: two shuffles, the sender picks the element (d[c & 1], then the other)
     by=[[None,None] for _ in range(32)]
-    for l in range(32):
-      r,c=l>>2,l&3
-      for ks in range(2):
-        ns=2*ks+(c>>1)+4*(c&1); src=Ip(r)*4+(ns>>1)
-        by[l][ks]=dx[src][ns&1]
+    for sh in range(2):
+      send=[dx[l][((l&3)&1)^sh] for l in range(32)]
+      for l in range(32):
+        r,c=l>>2,l&3
+        src=Ip(r)*4+([0,2,1,3] if sh==0 else [1,3,0,2])[c]
+        ks=(c>>1) if sh==0 else 1-(c>>1)
+        by[l][ks]=send[src]
     dy=dmma(M[1],by)
     for e in range(2):
       ad=[k*RP+(l>>2)*RS+Ip(2*(l&3)+e) for l in range(32)]
@@ -70,10 +73,15 @@ for w in range(4):
     dz=dmma(M[2],bz)
     for l in range(32):
       for e in range(2): dz[l][e]*=scale[l>>2][j][2*(l&3)+e]
+    # z -> z': two shuffles, sender element d[lane/4 >= 4], then the other
     bz2=[[None,None] for _ in range(32)]
-    for l in range(32):
-      r,c=l>>2,l&3; ir=Ip(r)
-      for ks in range(2): bz2[l][ks]=dz[(4*ks+c)*4+(ir>>1)][ir&1]
+    for sh in range(2):
+      send=[dz[l][int((l>>2)>=4)^sh] for l in range(32)]
+      for l in range(32):
+        r,c=l>>2,l&3; ir=Ip(r); e=ir&1
+        rs=(4+c if e else c) if sh==0 else (c if e else 4+c)
+        ks=e if sh==0 else 1-e
+        bz2[l][ks]=send[rs*4+(ir>>1)]
     dz2=dmma(M[3],bz2)
     st[(w,tt)]=dz2
 for w in range(4):
@@ -92,7 +100,15 @@ for w in range(4):
       check('Y2 ld',ad)
       for l in range(32): by2[l][ks]=wc[ad[l]]
     dy2=dmma(M[4],by2)
-    bx2=[[dy2[(l>>2)*4+((4*ks+(l&3))>>1)][(l&3)&1] for ks in range(2)] for l in range(32)]
+    # y' -> x': two shuffles within the quad, sender element d[c >> 1], then the other
+    bx2=[[None,None] for _ in range(32)]
+    for sh in range(2):
+      send=[dy2[l][((l&3)>>1)^sh] for l in range(32)]
+      for l in range(32):
+        r,c=l>>2,l&3
+        cs=(c>>1)+2*((c&1)^sh)
+        ks=(c&1)^sh
+        bx2[l][ks]=send[r*4+cs]
     dx2=dmma(M[5],bx2)
     for e in range(2):
       check('relax hb',[(k+1)*HP+(2*(l&3)+e+1)*HS+(l>>2)+1 for l in range(32)])
