@@ -33,9 +33,9 @@ bool line_zgen_supported(int nx);
 cudaError_t launch_line_zgen(const int* nxs, int nnx, int unit, const PatchDev* patches, const unsigned char* active,
                              const StencilDev& st, double omega, double* partials, const void* units, int nunits,
                              int grid, const LineFac& L, cudaStream_t stream);
-cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
-                           const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
-                           const LineFac& L, cudaStream_t stream);
+cudaError_t launch_line_nx(int nx, int unit, const PatchDev& P, int act, const StencilDev& st, double omega,
+                           double* partials, long long t0, long long t1, int grid, const LineFac& L,
+                           cudaStream_t stream);
 cudaError_t launch_physical_ghosts(const PatchDev* patches, int npatch, const unsigned char* active,
                                    long long max_face, int skip_x, int use_covered, cudaStream_t stream);
 cudaError_t launch_interface_copies(const PatchDev* patches, const unsigned char* active, const CopyDev* copies,
@@ -742,8 +742,9 @@ static long long zmarch_min_cells() {
   return zmin;
 }
 
-static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, double* part, int pa, int pb, int ka,
-                        int kb, cudaStream_t s) {
+// da: the device copy of the active flags, ha: the host one
+static int sweep_planes(psm_plan* P, const unsigned char* da, const unsigned char* ha, double omega, double* part,
+                        int pa, int pb, int ka, int kb, cudaStream_t s) {
   const bool unit = P->st.xm == -1.0 && P->st.xp == -1.0 && P->st.ym == -1.0 && P->st.yp == -1.0 &&
                     P->st.zm == -1.0 && P->st.zp == -1.0;
   int p = pa;
@@ -767,8 +768,8 @@ static int sweep_planes(psm_plan* P, const unsigned char* da, double omega, doub
         const PatchDev& h = P->hp[r];
         const int a = ka, b = (kb < 0) ? h.nz : kb;
         const long long t0 = h.tile0 + (long long)a * h.tpp, t1 = h.tile0 + (long long)b * h.tpp;
-        CUDA_TRY(launch_line_nx(nx, unit ? 1 : 0, P->d_patches, P->npatch, da, P->st, omega, part, t0, t1,
-                                line_nx_occupancy(nx) * sms, P->fac[r]->h_line, s));
+        CUDA_TRY(launch_line_nx(nx, unit ? 1 : 0, h, ha[r], P->st, omega, part, t0, t1, line_nx_occupancy(nx) * sms,
+                                P->fac[r]->h_line, s));
         P->launches += 1;
       }
     } else if (P->tiled && line_nx_specialised(nx) && P->hp[p].R == zmarch_rows(nx)) {
@@ -879,7 +880,7 @@ int psm_jacobi_sweep(psm_plan* P, const unsigned char* active, double omega, int
   double* part = slot_ptr(P, slot, &rc);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (P->kind == PSM_BLOCK_LINE) return sweep_planes(P, da, omega, part, 0, P->npatch, 0, -1, s);
+  if (P->kind == PSM_BLOCK_LINE) return sweep_planes(P, da, active, omega, part, 0, P->npatch, 0, -1, s);
   if (P->kind != 0) P->phys_pending = std::max(P->phys_pending, 1);  // plane/box sweeps write x faces only
   if (P->kind == PSM_BLOCK_PLANE) return psm_plane_jacobi(P, da, omega, part, s);
   if (P->kind == PSM_BLOCK_BOX) {
@@ -915,7 +916,7 @@ int psm_jacobi_sweep_planes(psm_plan* P, const unsigned char* active, double ome
   double* part = slot_ptr(P, slot, &rc);
   if (rc) return rc;
   if (k1 == k0) return PSM_OK;
-  return sweep_planes(P, da, omega, part, patch, patch + 1, k0, k1, (cudaStream_t)stream);
+  return sweep_planes(P, da, active, omega, part, patch, patch + 1, k0, k1, (cudaStream_t)stream);
 }
 
 int psm_halo_unpack(psm_plan* P, const unsigned char* active, int patch, int side, const double* plane_dev,

@@ -268,8 +268,7 @@ __global__ void line_apply_kernel(const LineFac* __restrict__ L, const double* _
 #endif
 constexpr int kNxT = PSM_NX_THREADS;  // threads per tile CTA (cells per thread: 2048 / kNxT)
 template <int NX, int UNIT>
-__global__ void __launch_bounds__(kNxT, 512 / kNxT) line_jacobi_nx_kernel(const PatchDev* __restrict__ patches, int npatch,
-                                                                const unsigned char* __restrict__ active,
+__global__ void __launch_bounds__(kNxT, 512 / kNxT) line_jacobi_nx_kernel(const __grid_constant__ PatchDev P, int act,
                                                                 StencilDev st, double omega,
                                                                 double* __restrict__ partials, long long tile_begin,
                                                                 long long tile_end, const __grid_constant__ LineFac L) {
@@ -281,8 +280,9 @@ __global__ void __launch_bounds__(kNxT, 512 / kNxT) line_jacobi_nx_kernel(const 
   __shared__ double wsum[2][T / 32];
   __shared__ double tab_invm[kSeg], tab_loinv[kSeg], tab_cp[kSeg], tab_g[kSeg], tab_h[kSeg];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // the line factors come in as a kernel parameter (constant bank): no
-  // global round trip before the first tile
+  // the patch (one launch per patch), its active buffer and the line factors
+  // come in as kernel parameters (constant bank): no global round trip
+  // before the first tile's loads
   if (tid < kSeg) {
     const double im = L.invm[tid];
     tab_invm[tid] = im;
@@ -302,19 +302,12 @@ __global__ void __launch_bounds__(kNxT, 512 / kNxT) line_jacobi_nx_kernel(const 
 #ifdef PSM_NX_TIMING
     if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm0));
 #endif
-    const int pi = find_patch(patches, npatch, tile);
-    const PatchDev& P = patches[pi];
-    // independent loads first (the tile's latency is a chain of L2 round
-    // trips at small sizes): the active flag and both buffer pointers
-    const int act = active[pi];
-    double* const b0 = P.buf[0];
-    double* const b1 = P.buf[1];
     const int ny = P.ny;
     int k, j0, rows;
     tile_coords(P, tile, k, j0, rows);
     const long long pxy = (long long)PX * (ny + 2);
-    const double* __restrict__ u = act ? b1 : b0;
-    double* __restrict__ v = act ? b0 : b1;
+    const double* __restrict__ u = P.buf[act];
+    double* __restrict__ v = P.buf[act ^ 1];
     const long long ubase = (long long)(k + 1) * pxy + (long long)(j0 + 1) * PX + 1;
     const double* __restrict__ fb = P.f + ((long long)k * ny + j0) * NX;
     double* __restrict__ rb = rs[buf];
@@ -455,13 +448,13 @@ __global__ void __launch_bounds__(kNxT, 512 / kNxT) line_jacobi_nx_kernel(const 
 }
 
 template <int NX>
-static cudaError_t launch_nx(int unit, const PatchDev* patches, int npatch, const unsigned char* active,
-                             const StencilDev& st, double omega, double* partials, long long t0, long long t1,
-                             int grid, const LineFac& L, cudaStream_t stream) {
+static cudaError_t launch_nx(int unit, const PatchDev& P, int act, const StencilDev& st, double omega,
+                             double* partials, long long t0, long long t1, int grid, const LineFac& L,
+                             cudaStream_t stream) {
   if (unit)
-    line_jacobi_nx_kernel<NX, 1><<<grid, kNxT, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1, L);
+    line_jacobi_nx_kernel<NX, 1><<<grid, kNxT, 0, stream>>>(P, act, st, omega, partials, t0, t1, L);
   else
-    line_jacobi_nx_kernel<NX, 0><<<grid, kNxT, 0, stream>>>(patches, npatch, active, st, omega, partials, t0, t1, L);
+    line_jacobi_nx_kernel<NX, 0><<<grid, kNxT, 0, stream>>>(P, act, st, omega, partials, t0, t1, L);
   return cudaGetLastError();
 }
 
@@ -491,14 +484,15 @@ int line_nx_occupancy(int nx) {
   }
 }
 
-cudaError_t launch_line_nx(int nx, int unit, const PatchDev* patches, int npatch, const unsigned char* active,
-                           const StencilDev& st, double omega, double* partials, long long t0, long long t1, int grid,
-                           const LineFac& L, cudaStream_t stream) {
+// tiles [t0, t1) of patch P (host copy of its descriptor), active buffer act
+cudaError_t launch_line_nx(int nx, int unit, const PatchDev& P, int act, const StencilDev& st, double omega,
+                           double* partials, long long t0, long long t1, int grid, const LineFac& L,
+                           cudaStream_t stream) {
   if (t1 <= t0) return cudaSuccess;
   const long long n = t1 - t0;
   if (grid > n) grid = (int)n;
 #define PSM_NX(N) \
-  case N: return launch_nx<N>(unit, patches, npatch, active, st, omega, partials, t0, t1, grid, L, stream);
+  case N: return launch_nx<N>(unit, P, act, st, omega, partials, t0, t1, grid, L, stream);
   switch (nx) {
     PSM_NX(64)
     PSM_NX(128)

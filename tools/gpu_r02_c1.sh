@@ -1,12 +1,9 @@
 #!/bin/bash
-# nx line kernel (512 threads, factors as a kernel parameter): tests, C1/F3 timing, phase timings
+# small-level line Jacobi (patch + active flag as kernel parameters): tests, C1 latency, F3
 export PATCHSMOOTH_MAX_CELLS=${PATCHSMOOTH_MAX_CELLS:-100000000000}
 O=gpurun_out; mkdir -p $O
 make -j all > $O/build.log 2>&1 || { echo build failed; tail $O/build.log; exit 1; }
-timeout -s KILL 900 python -m pytest tests -m gpu -x -q -k "line or c1 or C1 or f3 or mixed or smoke" > $O/line_tests.log 2>&1; echo "line tests rc=$?"; tail -2 $O/line_tests.log
-timeout -s KILL 300 python tools/bench_configs.py --only C1 > $O/c1.jsonl 2>&1; cut -c150-400 $O/c1.jsonl
-timeout -s KILL 300 python tools/bench_configs.py --only F3 --runs 0 > $O/f3.jsonl 2>&1; cut -c150-400 $O/f3.jsonl
-mkdir -p build/variant
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DPSM_NX_TIMING -c -o build/variant/psm_line_t.o paper_1208_1975_b200/csrc/psm_line.cu && \
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variant/libpsmooth_t.so $(ls build/obj/*.o | grep -v psm_line.o) build/variant/psm_line_t.o -lcudart && \
-PSM_LIB=$PWD/build/variant/libpsmooth_t.so python tools/nx_timing_probe.py 2>&1 | tail -6
+timeout -s KILL 900 python -m pytest tests -m gpu -x -q -k "line or c1 or C1 or f3 or mixed or smoke or dist or api" > $O/line_tests.log 2>&1; echo "line tests rc=$?"; tail -2 $O/line_tests.log
+timeout -s KILL 300 python tools/latency_probe.py 64 line 2>&1 | head -4
+timeout -s KILL 300 python tools/bench_configs.py --only C1 2>&1 | cut -c150-400
+timeout -s KILL 300 python tools/bench_configs.py --only F3 --runs 0 2>&1 | cut -c150-400
