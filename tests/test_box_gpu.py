@@ -1,8 +1,10 @@
 """Box blocks (the paper's cubic blocks, DEFAULT_BLOCK_SIZES 2^3..8^3): the
 separable exact inverse (psm_box.cu) against the restatement's dense
 inverses (the reference's invert_dense + matvec form) at sizes beyond the
-golden fixtures; Jacobi and lexicographic GS iterates and histories within
-1e-12; the explicit inverse equals the dense one."""
+golden fixtures (odd widths: cp.async staging; even widths: TMA staging;
+a 240-block GS sweep through the ticket pipeline); Jacobi and lexicographic
+GS iterates and histories within 1e-12; the explicit inverse equals the
+dense one."""
 
 import numpy as np
 import pytest
@@ -36,6 +38,32 @@ def test_default_block_sizes_match_dense_restatement(block, scheme):
     o, g = _pair(shape, seed=sum(block))
     want = R.smooth(o, scheme, block, steps=2, exact_norm=False)
     cfg = ps.SmootherConfig(scheme=scheme, block_dims=block, steps=2)
+    _, hist = ps.smooth(g, cfg, ps.InverseCache())
+    assert G.rel_maxnorm(g.patches[0].u.cpu().numpy(), o.patches[0].u) < TOL
+    assert G.hist_rel(hist, want) < TOL
+
+
+@pytest.mark.parametrize("block", SIZES)
+@pytest.mark.parametrize("scheme", ["block_jacobi", "chaotic_block_gs"])
+def test_default_block_sizes_even_width_tma_staging(block, scheme):
+    """Even nx: 8^3 regions stage through TMA tensor copies (odd nx above
+    takes the cp.async fallback); y and z still truncate."""
+    shape = (24, 18, 14)
+    o, g = _pair(shape, seed=3 + sum(block))
+    want = R.smooth(o, scheme, block, steps=2, exact_norm=False)
+    cfg = ps.SmootherConfig(scheme=scheme, block_dims=block, steps=2)
+    _, hist = ps.smooth(g, cfg, ps.InverseCache())
+    assert G.rel_maxnorm(g.patches[0].u.cpu().numpy(), o.patches[0].u) < TOL
+    assert G.hist_rel(hist, want) < TOL
+
+
+def test_box_gs_many_blocks_ticket_pipeline():
+    """8^3 GS over 240 blocks (many CTAs, each holding two tickets, halos
+    prefetched as soon as the predecessors are done): still exactly the
+    lexicographic sweep."""
+    o, g = _pair((64, 40, 48), seed=17)
+    want = R.smooth(o, "chaotic_block_gs", (8, 8, 8), steps=2, exact_norm=False)
+    cfg = ps.SmootherConfig(scheme="chaotic_block_gs", block_dims=(8, 8, 8), steps=2)
     _, hist = ps.smooth(g, cfg, ps.InverseCache())
     assert G.rel_maxnorm(g.patches[0].u.cpu().numpy(), o.patches[0].u) < TOL
     assert G.hist_rel(hist, want) < TOL
