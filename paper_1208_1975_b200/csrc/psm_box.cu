@@ -372,7 +372,9 @@ __global__ void __launch_bounds__(kBoxT, PSM_BOX_MINB) box_sweep_t(const PatchDe
   // unfinished ticket's predecessors are held by CTAs that make progress.
   const bool gpre = gsp && tma;
   auto gs_acquire = [&]() {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // acquire pattern with the relaxed flag loads (fence.acquire: an L1
+    // invalidate only, no wait for this thread's own outstanding stores)
+    asm volatile("fence.acquire.gpu;" ::: "memory");
     // the TMA reads of the halo go through the async proxy
     if (tma) asm volatile("fence.proxy.async.global;" ::: "memory");
   };

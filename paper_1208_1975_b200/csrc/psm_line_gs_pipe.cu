@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC, MS>::MINB)
               seen_k1 = ld_relaxed_gpu(flag_k1);
               if (seen_k1 < need_k1) sg.check();
             }
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("fence.acquire.gpu;" ::: "memory");  // acquire pattern with the relaxed loads
           }
         }
         __syncwarp();
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kGsThreads, GCfg<NC, MS>::MINB)
             if (avail <= j) {
               SpinGuard sg;
               while ((avail = ld_relaxed_gpu(dep_flag)) <= j) sg.check();
-              if (!CHAOTIC || MS) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              if (!CHAOTIC || MS) asm volatile("fence.acquire.gpu;" ::: "memory");  // (acquire pattern)
               asm volatile("fence.proxy.async.global;" ::: "memory");
             }
             const int lim = min(avail, j + DM);
