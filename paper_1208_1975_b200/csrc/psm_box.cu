@@ -21,16 +21,20 @@
 //
 // Kernel: one 128-thread CTA per region of <= 8^3 cells tiled by whole
 // blocks (small blocks are batched, 2^3 blocks 64 to a region), persistent
-// over a region list.  The region's u with a one-cell halo is staged in
-// shared memory, the residual is formed in the reference operation order,
-// each 1-D transform has one thread per block line (line in registers, padded
-// rows: conflict-free), the 1/lambda scaling (host table per extent triple) is
-// folded into the last forward pass and the relaxation into the last
-// backward pass.  Jacobi writes v (and v's physical x-ghosts) for all
-// blocks in one launch; GS updates u in place one wavefront
-// (bi + bj + bk = w) of blocks per launch: face-adjacent blocks lie on
-// neighbouring wavefronts, so the order is exactly the lexicographic one of
-// runtime.py:164-168.
+// over a region list, six CTAs per SM.  The region's u with a one-cell halo
+// and its f are staged in shared memory (TMA tensor copies, double-buffered;
+// cp.async for odd widths), the residual is formed in the reference
+// operation order.  Interior 8^3 regions run the six 1-D transforms as DMMA
+// m8n8k4 passes with the data in fragment registers (box_sweep_t, below);
+// edge regions run them with one thread per block line.  The 1/lambda
+// scaling (host table per extent triple) is folded into the last forward
+// pass and the relaxation into the last backward pass.  Jacobi writes v (and
+// v's physical x-ghosts) for all blocks in one launch.  GS updates u in
+// place in one persistent launch per sweep: blocks are handed out in
+// wavefront order (bi + bj + bk = w; face-adjacent blocks lie on
+// neighbouring wavefronts) and each waits for its three lexicographic
+// predecessors' flags, so the order is exactly the lexicographic one of
+// runtime.py:164-168 (PSM_BOX_GS_WAVES=1: one launch per wavefront).
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
